@@ -1,0 +1,180 @@
+/*
+ * dvsg.h -- C-ABI of the B200-native batched graph search (libdvsg.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * exposes the path as C++ free functions (paths relative to
+ * /root/reference/proj):
+ *
+ *   beam_search_stats / beam_search / visited_count   include/dvs/graph_index.hpp:58-65
+ *   combine_results                                   include/dvs/simulator.hpp:66-67
+ *   run_pipeline (functional part)                    include/dvs/simulator.hpp:98-102
+ *   assign_top_c / partition_database                 include/dvs/kmeans.hpp:41-46
+ *   place_clusters / route                            include/dvs/router.hpp:53-57
+ *   compute_entry_order / build_graph                 include/dvs/graph_index.hpp:40-45
+ *   load_index / save_index (FNSY v1)                 include/dvs/index_file.hpp:13-14
+ *
+ * Every entry point below replaces one of those (cited per function), with
+ * plain pointers and sizes, caller-owned buffers, and no C++/torch types.
+ * INTEGRATION.md shows the C++ shim a maintainer binds in their place.
+ *
+ * Errors: status codes mirror the reference CLI's exit-code map
+ * (src/commands.cpp:355-361): DVSG_EINVAL <-> std::invalid_argument /
+ * config_error (2), DVSG_EFORMAT <-> format_error (3), DVSG_EINTERNAL <->
+ * internal_error and every CUDA error (4).  dvsg_last_error() returns the
+ * message of the last failing call on the calling thread.
+ *
+ * Threading: one host thread per context.  A context owns one CUDA device,
+ * its device-resident index and two streams (compute, comm).
+ */
+#ifndef DVSG_H
+#define DVSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int dvsg_status;
+#define DVSG_OK 0
+#define DVSG_EINVAL 2
+#define DVSG_EFORMAT 3
+#define DVSG_EINTERNAL 4
+
+#define DVSG_METRIC_L2 0 /* squared_l2, distance.cpp:19-27 */
+#define DVSG_METRIC_IP 1 /* -dot (distance.cpp:35-42); extension, parity unpinned */
+
+#define DVSG_ACCUM_F64 0 /* fp64 lane partials + fp64 tree, rounded once to f32 (parity mode) */
+#define DVSG_ACCUM_F32 1 /* fp32 lane partials + fp32 tree (fast mode) */
+
+typedef struct dvsg_ctx dvsg_ctx;
+
+/* SearchParams, include/dvs/graph_index.hpp:27-32, plus the metric and
+ * accumulation mode of the B200 kernel. */
+typedef struct {
+  int iterations;  /* I */
+  int beam_width;  /* w */
+  int k;
+  int entry_count; /* entry nodes; the reference CLI defaults it to w (config.cpp:226) */
+  int metric;      /* DVSG_METRIC_* */
+  int accum;       /* DVSG_ACCUM_* */
+} dvsg_search_params;
+
+const char *dvsg_last_error(void);
+const char *dvsg_version(void);
+
+/* ---- context ------------------------------------------------------------ */
+dvsg_status dvsg_create(int device, dvsg_ctx **out);
+dvsg_status dvsg_destroy(dvsg_ctx *ctx);
+/* the compute stream (cudaStream_t) so callers can time on it */
+void *dvsg_stream(dvsg_ctx *ctx);
+dvsg_status dvsg_synchronize(dvsg_ctx *ctx);
+
+/* ---- index load / partition  (load_index index_file.cpp:149-296,
+ *      BuiltIndex index.hpp:14-23, GraphIndex graph_index.hpp:13-25) ------- */
+
+/* Drops every partition and the centroids held by the context. */
+dvsg_status dvsg_index_reset(dvsg_ctx *ctx);
+/* Sets the routing table: centroids (clusters x dim) and placement
+ * (cluster_to_rank, router.cpp:28-43) for `ranks` ranks. */
+dvsg_status dvsg_set_centroids(dvsg_ctx *ctx, const float *centroids, int clusters, int dim,
+                               const uint32_t *cluster_to_rank, int ranks);
+/* Uploads one partition (a GraphIndex).  Host arrays are copied; the caller
+ * keeps ownership.  entry_order may be NULL, in which case it is computed
+ * exactly as compute_entry_order (graph_index.cpp:21-44).  adjacency rows hold
+ * local ids (n x out_degree); global_ids may be NULL (iota). */
+dvsg_status dvsg_load_partition(dvsg_ctx *ctx, uint32_t cluster, uint64_t n, int dim,
+                                int out_degree, const float *vectors,
+                                const uint32_t *adjacency, const uint32_t *global_ids,
+                                const uint32_t *entry_order);
+/* FNSY v1 (index_file.cpp:16-25, :149-296): loads the routing table and the
+ * partitions owned by `rank` (all partitions when rank < 0). */
+dvsg_status dvsg_load_index_file(dvsg_ctx *ctx, const char *path, int rank);
+/* FNSY v1 writer (index_file.cpp:88-147) over caller arrays: cluster c owns
+ * rows [offsets[c], offsets[c+1]) of vectors / adjacency / global_ids. */
+dvsg_status dvsg_save_index_file(const char *path, int clusters, int dim, int out_degree,
+                                 const float *centroids, const uint32_t *cluster_to_rank,
+                                 int ranks, const uint64_t *offsets, const float *vectors,
+                                 const uint32_t *adjacency, const uint32_t *global_ids);
+/* Shape of the loaded index: number of partitions resident on this context,
+ * dims, and the partition -> cluster id map (array of nparts, may be NULL). */
+dvsg_status dvsg_index_info(dvsg_ctx *ctx, int *nparts, int *dim, int *out_degree,
+                            int *clusters, uint32_t *cluster_ids, uint64_t *sizes);
+/* Downloads one resident partition's entry order (n u32) for checking. */
+dvsg_status dvsg_get_entry_order(dvsg_ctx *ctx, uint32_t cluster, uint32_t *out);
+
+/* compute_entry_order, graph_index.cpp:21-44 (host, exact) */
+dvsg_status dvsg_compute_entry_order(const float *vectors, uint64_t n, int dim, uint32_t *out);
+
+/* ---- the search (beam_search_stats, graph_index.cpp:105-187) ------------ */
+
+/* Batched beam_search_stats of nq queries against one resident partition.
+ * Host buffers.  out_ids/out_dists: nq x k, ascending (dist, global id);
+ * out_count[q] <= k (ragged); out_visited[q] = the reference's scored count. */
+dvsg_status dvsg_beam_search(dvsg_ctx *ctx, uint32_t cluster, const float *queries,
+                             uint64_t nq, int dim, const dvsg_search_params *p,
+                             uint32_t *out_ids, float *out_dists, uint32_t *out_count,
+                             uint64_t *out_visited);
+
+/* Device-pointer variant over an explicit unit list: unit u searches query
+ * unit_query[u] (row of d_queries, nq x dim) in partition unit_cluster[u].
+ * All pointers are device pointers on this context's device; runs on the
+ * compute stream, asynchronous. */
+dvsg_status dvsg_search_units_device(dvsg_ctx *ctx, const float *d_queries, uint64_t nq,
+                                     int dim, const uint32_t *d_unit_query,
+                                     const uint32_t *d_unit_cluster, uint64_t nunits,
+                                     const dvsg_search_params *p, uint32_t *d_out_ids,
+                                     float *d_out_dists, uint32_t *d_out_count,
+                                     uint64_t *d_out_visited);
+
+/* ---- routing and merge -------------------------------------------------- */
+
+/* assign_top_c, kmeans.cpp:243-280, on the GPU against the context's
+ * centroids.  Host buffers; out is nq x c cluster ids. */
+dvsg_status dvsg_assign_top_c(dvsg_ctx *ctx, const float *queries, uint64_t nq, int dim,
+                              int c, uint32_t *out);
+
+/* combine_results, simulator.cpp:219-243, on the GPU.  nq queries, each with
+ * nparts partial lists of <= stride entries (counts nq x nparts); out nq x k. */
+dvsg_status dvsg_combine_results(dvsg_ctx *ctx, uint64_t nq, int nparts, const uint32_t *ids,
+                                 const float *dists, const uint32_t *counts, int stride, int k,
+                                 uint32_t *out_ids, float *out_dists, uint32_t *out_count);
+
+/* ---- run_pipeline functional part (simulator.cpp:245-337), one GPU ------
+ * assign (K5) -> route -> search (K1) -> combine (K4) -> attach hit vectors.
+ * All clusters must be resident on this context.  Host buffers;
+ * out_vectors (nq x k x dim) may be NULL; visited_total may be NULL. */
+dvsg_status dvsg_run_pipeline(dvsg_ctx *ctx, const float *queries, uint64_t nq, int dim,
+                              const dvsg_search_params *p, int fanout, int ranks,
+                              int batch_index, uint32_t *out_ids, float *out_dists,
+                              uint32_t *out_count, float *out_vectors, uint64_t *visited_total);
+/* Same, device pointers, asynchronous on the compute stream.  d_visited is
+ * per (query, fanout slot) (nq x fanout) and may be NULL. */
+dvsg_status dvsg_run_pipeline_device(dvsg_ctx *ctx, const float *d_queries, uint64_t nq,
+                                     int dim, const dvsg_search_params *p, int fanout,
+                                     uint32_t *d_out_ids, float *d_out_dists,
+                                     uint32_t *d_out_count, float *d_out_vectors,
+                                     uint64_t *d_visited);
+
+/* ---- graph build (build_graph, graph_index.cpp:46-97) -------------------
+ * Exact kNN rows (ties by lower id) on the GPU over a host partition; the
+ * distance is fp32 over (x-y)^2, exact for integer-valued data (SIFT-like
+ * bytes), within fp32 rounding otherwise.  adjacency_out: n x out_degree. */
+dvsg_status dvsg_build_graph(dvsg_ctx *ctx, const float *vectors, uint64_t n, int dim,
+                             int out_degree, uint32_t *adjacency_out);
+
+/* ---- instrumentation ---------------------------------------------------- */
+/* Device time (ms) of the last search kernel launch (K1) and of the whole
+ * last pipeline call, measured with CUDA events on the compute stream;
+ * enable with dvsg_set_timing(ctx, 1). */
+dvsg_status dvsg_set_timing(dvsg_ctx *ctx, int enabled);
+dvsg_status dvsg_last_timings(dvsg_ctx *ctx, float *search_ms, float *assign_ms,
+                              float *combine_ms, float *total_ms);
+/* Number of library kernels launched by this context since creation. */
+uint64_t dvsg_kernel_launches(dvsg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

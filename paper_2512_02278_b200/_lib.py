@@ -1,0 +1,112 @@
+"""ctypes binding of libdvsg.so -- the C-ABI declared in include/dvsg.h.
+
+The library is built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).
+There is no fallback: if the shared object is missing this module raises at
+import time, so no caller can silently run anything but the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_float, c_int, c_uint32, c_uint64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdvsg.so")
+
+if not os.path.isfile(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the B200 search path has no CPU fallback)")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+DVSG_OK, DVSG_EINVAL, DVSG_EFORMAT, DVSG_EINTERNAL = 0, 2, 3, 4
+METRIC_L2, METRIC_IP = 0, 1
+ACCUM_F64, ACCUM_F32 = 0, 1
+
+
+class dvsg_search_params(ctypes.Structure):
+    _fields_ = [("iterations", c_int), ("beam_width", c_int), ("k", c_int),
+                ("entry_count", c_int), ("metric", c_int), ("accum", c_int)]
+
+
+P_u32 = POINTER(c_uint32)
+P_f32 = POINTER(c_float)
+P_u64 = POINTER(c_uint64)
+P_params = POINTER(dvsg_search_params)
+
+_SIGS = {
+    "dvsg_last_error": (c_char_p, []),
+    "dvsg_version": (c_char_p, []),
+    "dvsg_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "dvsg_destroy": (c_int, [c_void_p]),
+    "dvsg_stream": (c_void_p, [c_void_p]),
+    "dvsg_synchronize": (c_int, [c_void_p]),
+    "dvsg_index_reset": (c_int, [c_void_p]),
+    "dvsg_set_centroids": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_int]),
+    "dvsg_load_partition": (c_int, [c_void_p, c_uint32, c_uint64, c_int, c_int, c_void_p,
+                                    c_void_p, c_void_p, c_void_p]),
+    "dvsg_load_index_file": (c_int, [c_void_p, c_char_p, c_int]),
+    "dvsg_save_index_file": (c_int, [c_char_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                                     c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dvsg_index_info": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int),
+                                POINTER(c_int), c_void_p, c_void_p]),
+    "dvsg_get_entry_order": (c_int, [c_void_p, c_uint32, c_void_p]),
+    "dvsg_compute_entry_order": (c_int, [c_void_p, c_uint64, c_int, c_void_p]),
+    "dvsg_beam_search": (c_int, [c_void_p, c_uint32, c_void_p, c_uint64, c_int, P_params,
+                                 c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dvsg_search_units_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_void_p,
+                                         c_uint64, P_params, c_void_p, c_void_p, c_void_p,
+                                         c_void_p]),
+    "dvsg_assign_top_c": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
+    "dvsg_combine_results": (c_int, [c_void_p, c_uint64, c_int, c_void_p, c_void_p, c_void_p,
+                                     c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "dvsg_run_pipeline": (c_int, [c_void_p, c_void_p, c_uint64, c_int, P_params, c_int, c_int,
+                                  c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dvsg_run_pipeline_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, P_params, c_int,
+                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dvsg_build_graph": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
+    "dvsg_set_timing": (c_int, [c_void_p, c_int]),
+    "dvsg_last_timings": (c_int, [c_void_p, P_f32, P_f32, P_f32, P_f32]),
+    "dvsg_kernel_launches": (c_uint64, [c_void_p]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+class DvsError(RuntimeError):
+    """Base class; ``code`` is the dvsg status (2/3/4, commands.cpp:355-361)."""
+
+    code = DVSG_EINTERNAL
+
+
+class InvalidArgument(DvsError, ValueError):
+    """std::invalid_argument / config_error in the reference (exit code 2)."""
+
+    code = DVSG_EINVAL
+
+
+class FormatError(DvsError):
+    """format_error in the reference (exit code 3)."""
+
+    code = DVSG_EFORMAT
+
+
+class InternalError(DvsError):
+    """internal_error and every CUDA failure (exit code 4)."""
+
+    code = DVSG_EINTERNAL
+
+
+_BY_CODE = {DVSG_EINVAL: InvalidArgument, DVSG_EFORMAT: FormatError, DVSG_EINTERNAL: InternalError}
+
+
+def check(status: int) -> None:
+    if status != DVSG_OK:
+        msg = lib.dvsg_last_error().decode("utf-8", "replace")
+        raise _BY_CODE.get(status, InternalError)(msg)

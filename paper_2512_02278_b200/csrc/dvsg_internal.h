@@ -1,0 +1,79 @@
+// dvsg_internal.h -- shared device-side definitions of libdvsg (not public API).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dvsg {
+
+constexpr int kThreads = 256;        // K1 CTA size (8 warps)
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+// One resident partition (a GraphIndex, graph_index.hpp:13-25) inside the
+// context's concatenated device arrays: rows [row_off, row_off + n) of
+// vectors (dpad floats per row, 16-B aligned), adjacency (dg local ids per
+// row), global ids and entry order.
+struct PartDesc {
+  uint64_t row_off;
+  uint32_t n;
+  uint32_t cluster;
+};
+
+struct SearchArgs {
+  const float* vectors;       // rows x dpad
+  const uint32_t* adjacency;  // rows x dg
+  const uint32_t* gids;       // rows
+  const uint32_t* entry;      // rows (per-partition entry order)
+  const PartDesc* parts;      // partition slots
+  const float* queries;       // nq x dim (unpadded)
+  uint64_t nq;
+  const uint32_t* unit_query;  // nunits
+  const uint32_t* unit_part;   // nunits (partition slot)
+  uint64_t nunits;
+  int dim, dpad, dg;
+  int iters, beam, k, entry_count, cap;
+  int chp;      // survivor buffer entries (pow2 >= max(chunk, cap))
+  int hsize;    // visited hash slots (pow2)
+  uint32_t* hash_global;  // nullptr -> visited hash in shared memory
+  uint32_t* out_ids;      // nunits x k
+  float* out_dists;       // nunits x k
+  uint32_t* out_count;    // nunits
+  uint64_t* out_visited;  // nunits
+  unsigned long long* work_counter;
+};
+
+// Launch K1 (search_kernel.cu).  Returns a cudaError_t.
+// max_grid > 0 caps the persistent grid (one global hash region per CTA).
+cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sms,
+                          int max_grid, cudaStream_t stream, int* grid_out);
+// Shared-memory bytes K1 needs for these args (hash in smem when hash_global==nullptr).
+size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_smem);
+constexpr int kChunk = 2048;  // raw candidates per dedup/score/merge chunk (8 per thread)
+
+// K5 assign (route_kernels.cu): nq x c cluster ids, exact fp64 expanded form.
+cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const float* cents,
+                          const double* cent_norms, int clusters, int c, uint32_t* out,
+                          cudaStream_t stream);
+// K4 combine: per query merge nparts sorted partial lists (stride entries each).
+cudaError_t launch_combine(uint64_t nq, int nparts, const uint32_t* ids, const float* dists,
+                           const uint32_t* counts, int stride, int k, uint32_t* out_ids,
+                           float* out_dists, uint32_t* out_count, int* err_flag,
+                           cudaStream_t stream);
+// Route: build (unit_query, unit_part) from the assignment and the cluster->slot map.
+cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,
+                         const int32_t* cluster_to_slot, uint32_t* unit_query,
+                         uint32_t* unit_part, int* err_flag, cudaStream_t stream);
+// Attach hit vectors (simulator.cpp:329-333): gid -> (slot row) locator.
+cudaError_t launch_gather_vectors(const uint32_t* ids, const uint32_t* counts, uint64_t nq,
+                                  int k, const uint64_t* locator, const float* vectors,
+                                  int dim, int dpad, float* out, cudaStream_t stream);
+// Sum of per-unit visited counters.
+cudaError_t launch_reduce_u64(const uint64_t* in, uint64_t n, unsigned long long* out,
+                              cudaStream_t stream);
+
+// K6 exact kNN graph rows (knn_build.cu)
+cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad,
+                             int out_degree, uint32_t* adjacency, cudaStream_t stream);
+
+}  // namespace dvsg

@@ -1,0 +1,1019 @@
+// host.cpp -- C++ host layer + C-ABI of libdvsg.so (declared in include/dvsg.h).
+//
+// Keeps the reference's index-load / partition / search API
+// (/root/reference/proj/include/dvs/{graph_index,index,index_file,kmeans,
+// router,simulator}.hpp) and drives the sm_100a kernels in
+// search_kernel.cu (K1), route_kernels.cu (K4/K5) and knn_build.cu (K6).
+//
+// Device layout per context (one CUDA device):
+//   vectors   rows x dpad f32 (dpad = dim rounded up to 4: 16-B aligned rows,
+//             zero padded -- padding adds exact zeros to every distance)
+//   adjacency rows x out_degree u32 (partition-local ids)
+//   gids      rows u32, entry rows u32 (per-partition entry order)
+//   parts     PartDesc per resident partition (row offset, n, cluster id)
+// Partitions are appended; a partition never moves once uploaded except
+// when the arrays grow (one device-to-device copy).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/dvsg.h"
+#include "dvsg_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  throw Fail{code, buf};
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(DVSG_EINTERNAL, "%s: CUDA error %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+template <class F>
+dvsg_status guarded(F&& f) {
+  try {
+    f();
+    return DVSG_OK;
+  } catch (const Fail& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return DVSG_EINTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return DVSG_EINTERNAL;
+  }
+}
+
+// Growable device array.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  int device = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void reserve(size_t n, cudaStream_t s, bool keep = false, size_t keep_n = 0) {
+    if (n <= cap) return;
+    size_t nc = std::max(n, cap + cap / 2);
+    T* np = nullptr;
+    cuda_check(cudaMalloc(&np, nc * sizeof(T)), "cudaMalloc");
+    if (keep && p && keep_n) {
+      cuda_check(cudaMemcpyAsync(np, p, keep_n * sizeof(T), cudaMemcpyDeviceToDevice, s), "grow copy");
+      cuda_check(cudaStreamSynchronize(s), "grow sync");
+    }
+    if (p) cudaFree(p);
+    p = np;
+    cap = nc;
+  }
+};
+
+bool finite_all(const float* x, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i)
+    if (!std::isfinite(x[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+struct dvsg_ctx {
+  int device = 0;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t comm = nullptr;    // exchange
+  // index
+  int dim = 0, dpad = 0, dg = 0;
+  uint64_t rows = 0;
+  DevBuf<float> vec;
+  DevBuf<uint32_t> adj, gids, entry;
+  std::vector<dvsg::PartDesc> parts;
+  DevBuf<dvsg::PartDesc> d_parts;
+  bool parts_dirty = true;
+  // routing table
+  int clusters = 0, ranks = 1;
+  std::vector<float> cents;
+  std::vector<uint32_t> placement;
+  DevBuf<float> d_cents;
+  DevBuf<double> d_cent_norms;
+  DevBuf<int32_t> d_cluster_slot;
+  bool slot_dirty = true;
+  DevBuf<uint64_t> d_locator;
+  uint64_t locator_n = 0;
+  bool locator_dirty = true;
+  // scratch
+  DevBuf<uint32_t> unit_q, unit_p, assign;
+  DevBuf<uint32_t> u_ids, u_count;
+  DevBuf<float> u_dists;
+  DevBuf<uint64_t> u_visited;
+  DevBuf<uint32_t> hash;
+  DevBuf<unsigned long long> counter;
+  DevBuf<int> err_flag;
+  DevBuf<float> io_f;
+  DevBuf<uint32_t> io_u;
+  DevBuf<uint64_t> io_u64;
+  // timing
+  bool timing = false;
+  cudaEvent_t ev[8] = {};
+  float t_search = 0, t_assign = 0, t_combine = 0, t_total = 0;
+  std::atomic<uint64_t> launches{0};
+};
+
+namespace {
+
+void set_device(dvsg_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+int32_t slot_of(const dvsg_ctx* c, uint32_t cluster) {
+  for (size_t i = 0; i < c->parts.size(); ++i)
+    if (c->parts[i].cluster == cluster) return (int32_t)i;
+  return -1;
+}
+
+void sync_parts(dvsg_ctx* c) {
+  if (!c->parts_dirty) return;
+  c->d_parts.reserve(std::max<size_t>(c->parts.size(), 1), c->stream);
+  if (!c->parts.empty())
+    cuda_check(cudaMemcpyAsync(c->d_parts.p, c->parts.data(), c->parts.size() * sizeof(dvsg::PartDesc),
+                               cudaMemcpyHostToDevice, c->stream), "upload parts");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync parts");
+  c->parts_dirty = false;
+}
+
+void sync_slots(dvsg_ctx* c) {
+  if (!c->slot_dirty) return;
+  int n = c->clusters;
+  for (auto& p : c->parts) n = std::max<int>(n, (int)p.cluster + 1);
+  std::vector<int32_t> m((size_t)std::max(n, 1), -1);
+  for (size_t i = 0; i < c->parts.size(); ++i) m[c->parts[i].cluster] = (int32_t)i;
+  c->d_cluster_slot.reserve(m.size(), c->stream);
+  cuda_check(cudaMemcpyAsync(c->d_cluster_slot.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice, c->stream), "slots");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync slots");
+  c->slot_dirty = false;
+}
+
+// compute_entry_order, graph_index.cpp:21-44: fp64 column sums, f32 mean,
+// fp64 sequential squared_l2 to the mean rounded to f32, sort (dist, id).
+void entry_order_host(const float* v, uint64_t n, int dim, uint32_t* out) {
+  std::vector<double> sums((size_t)dim, 0.0);
+  for (uint64_t i = 0; i < n; ++i) {
+    const float* r = v + i * (uint64_t)dim;
+    for (int j = 0; j < dim; ++j) sums[(size_t)j] += r[j];
+  }
+  std::vector<float> mean((size_t)dim);
+  for (int j = 0; j < dim; ++j) mean[(size_t)j] = (float)(sums[(size_t)j] / (double)n);
+  std::vector<uint64_t> key(n);
+  auto body = [&](uint64_t b, uint64_t e) {
+    for (uint64_t i = b; i < e; ++i) {
+      const float* r = v + i * (uint64_t)dim;
+      double acc = 0.0;
+      for (int j = 0; j < dim; ++j) {
+        const double d = (double)r[j] - (double)mean[(size_t)j];
+        acc += d * d;
+      }
+      const float f = (float)acc;  // >= 0, so the raw bits order like the value
+      uint32_t bits;
+      std::memcpy(&bits, &f, 4);
+      key[i] = ((uint64_t)bits << 32) | (uint32_t)i;
+    }
+  };
+  const unsigned nt = std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+  if (n < 65536 || nt == 1) {
+    body(0, n);
+  } else {
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) th.emplace_back(body, n * t / nt, n * (t + 1) / nt);
+    for (auto& x : th) x.join();
+  }
+  std::sort(key.begin(), key.end());
+  for (uint64_t i = 0; i < n; ++i) out[i] = (uint32_t)key[i];
+}
+
+void validate_params(const dvsg_search_params* p) {
+  if (!p) fail(DVSG_EINVAL, "SearchParams: null");
+  if (p->iterations < 1 || p->beam_width < 1 || p->k < 1 || p->entry_count < 1)
+    fail(DVSG_EINVAL, "SearchParams: iterations, beam_width, k and entry_count must all be >= 1");
+  if (p->metric != DVSG_METRIC_L2 && p->metric != DVSG_METRIC_IP) fail(DVSG_EINVAL, "SearchParams: unknown metric %d", p->metric);
+  if (p->accum != DVSG_ACCUM_F64 && p->accum != DVSG_ACCUM_F32) fail(DVSG_EINVAL, "SearchParams: unknown accum %d", p->accum);
+}
+
+uint64_t pow2_at_least(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// Core: K1 over a device unit list.  All pointers device.
+void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uint32_t* d_uq,
+                  const uint32_t* d_up, uint64_t nunits, const dvsg_search_params* p,
+                  uint32_t* d_ids, float* d_dists, uint32_t* d_count, uint64_t* d_visited) {
+  validate_params(p);
+  if (c->parts.empty()) fail(DVSG_EINVAL, "beam_search: empty graph");
+  if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
+  if (nunits == 0) return;
+  if ((uint64_t)p->beam_width * (uint64_t)c->dg > (1ull << 30)) fail(DVSG_EINVAL, "beam_search: beam_width * out_degree too large");
+  sync_parts(c);
+  const uint64_t cap = std::max<uint64_t>(4ull * (uint64_t)p->k, 2ull * (uint64_t)p->iterations * (uint64_t)p->beam_width);
+  if (cap > (1ull << 20)) fail(DVSG_EINVAL, "beam_search: candidate pool capacity %llu exceeds the device limit", (unsigned long long)cap);
+  // visited never exceeds min(n_max, entries + I*w*dg)
+  uint64_t nmax = 0;
+  for (auto& pd : c->parts) nmax = std::max<uint64_t>(nmax, pd.n);
+  const uint64_t entries = std::min<uint64_t>((uint64_t)p->entry_count, nmax);
+  const uint64_t bound = std::min<uint64_t>(nmax, entries + (uint64_t)p->iterations * (uint64_t)p->beam_width * (uint64_t)c->dg);
+  const uint64_t hsize = std::max<uint64_t>(64, pow2_at_least(bound + 1));
+  const uint64_t chp = std::max<uint64_t>(pow2_at_least((uint64_t)dvsg::kChunk), pow2_at_least(cap));
+
+  static const uint64_t hash_smem_max = [] {
+    const char* e = std::getenv("DVSG_HASH_SMEM_MAX");
+    return e ? std::strtoull(e, nullptr, 10) : 16384ull;
+  }();
+  bool in_smem = hsize <= hash_smem_max;
+  size_t smem = dvsg::search_smem_bytes((int)cap, (int)chp, p->beam_width, (int)hsize, in_smem);
+  if (in_smem && smem > c->smem_optin) in_smem = false;
+  smem = dvsg::search_smem_bytes((int)cap, (int)chp, p->beam_width, (int)hsize, in_smem);
+  if (smem > c->smem_optin) fail(DVSG_EINVAL, "beam_search: pool (%llu) too large for shared memory", (unsigned long long)cap);
+
+  dvsg::SearchArgs a{};
+  a.vectors = c->vec.p;
+  a.adjacency = c->adj.p;
+  a.gids = c->gids.p;
+  a.entry = c->entry.p;
+  a.parts = c->d_parts.p;
+  a.queries = d_q;
+  a.nq = nq;
+  a.unit_query = d_uq;
+  a.unit_part = d_up;
+  a.nunits = nunits;
+  a.dim = dim;
+  a.dpad = c->dpad;
+  a.dg = c->dg;
+  a.iters = p->iterations;
+  a.beam = p->beam_width;
+  a.k = p->k;
+  a.entry_count = p->entry_count;
+  a.cap = (int)cap;
+  a.chp = (int)chp;
+  a.hsize = (int)hsize;
+  a.out_ids = d_ids;
+  a.out_dists = d_dists;
+  a.out_count = d_count;
+  a.out_visited = d_visited;
+  c->counter.reserve(1, c->stream);
+  a.work_counter = c->counter.p;
+  cuda_check(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned long long), c->stream), "counter reset");
+  int max_grid = 0;
+  if (!in_smem) {
+    // one L2-resident region per persistent CTA
+    max_grid = 4 * c->num_sms;
+    c->hash.reserve((uint64_t)max_grid * hsize, c->stream);
+    a.hash_global = c->hash.p;
+  }
+  if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+  int grid = 0;
+  cuda_check(dvsg::launch_search(a, p->metric, p->accum, c->num_sms, max_grid, c->stream, &grid), "search kernel launch");
+  if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+  c->launches += 1;
+}
+
+template <class T>
+T* stage(DevBuf<T>& b, const T* host, size_t n, cudaStream_t s) {
+  b.reserve(std::max<size_t>(n, 1), s);
+  if (n) cuda_check(cudaMemcpyAsync(b.p, host, n * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+  return b.p;
+}
+
+void build_locator(dvsg_ctx* c) {
+  if (!c->locator_dirty) return;
+  // gid -> device row, over the resident partitions (simulator.cpp:275-288)
+  std::vector<uint32_t> g(c->rows);
+  if (c->rows) cuda_check(cudaMemcpy(g.data(), c->gids.p, c->rows * 4, cudaMemcpyDeviceToHost), "gids D2H");
+  uint64_t total = 0;
+  for (auto x : g) total = std::max<uint64_t>(total, (uint64_t)x + 1);
+  std::vector<uint64_t> loc(std::max<uint64_t>(total, 1), ~0ull);
+  for (uint64_t r = 0; r < c->rows; ++r) {
+    if (loc[g[r]] != ~0ull) fail(DVSG_EINTERNAL, "run_pipeline: partitions do not form a dense id cover");
+    loc[g[r]] = r;
+  }
+  c->d_locator.reserve(loc.size(), c->stream);
+  cuda_check(cudaMemcpyAsync(c->d_locator.p, loc.data(), loc.size() * 8, cudaMemcpyHostToDevice, c->stream), "locator");
+  cuda_check(cudaStreamSynchronize(c->stream), "locator sync");
+  c->locator_n = total;
+  c->locator_dirty = false;
+}
+
+void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const dvsg_search_params* p,
+                     int fanout, uint32_t* d_ids, float* d_dists, uint32_t* d_count, float* d_vecs,
+                     uint64_t* d_visited) {
+  validate_params(p);
+  if (c->clusters < 1) fail(DVSG_EINVAL, "BuiltIndex: index is not built");
+  if (dim != c->dim) fail(DVSG_EINVAL, "run_pipeline: query dim %d != index dim %d", dim, c->dim);
+  if (fanout < 1 || fanout > c->clusters)
+    fail(DVSG_EINVAL, "run_pipeline: fanout %d out of range for %d clusters", fanout, c->clusters);
+  if (fanout > 32) fail(DVSG_EINVAL, "run_pipeline: fanout %d above the device merge width 32", fanout);
+  if (nq == 0) return;
+  sync_slots(c);
+  const uint64_t nu = nq * (uint64_t)fanout;
+  c->assign.reserve(nu, c->stream);
+  c->unit_q.reserve(nu, c->stream);
+  c->unit_p.reserve(nu, c->stream);
+  c->u_ids.reserve(nu * (uint64_t)p->k, c->stream);
+  c->u_dists.reserve(nu * (uint64_t)p->k, c->stream);
+  c->u_count.reserve(nu, c->stream);
+  uint64_t* vis = d_visited;
+  if (!vis) {
+    c->u_visited.reserve(nu, c->stream);
+    vis = c->u_visited.p;
+  }
+  c->err_flag.reserve(1, c->stream);
+  cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+  if (c->timing) cudaEventRecord(c->ev[2], c->stream);
+  cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->stream), "assign");
+  cuda_check(dvsg::launch_route(c->assign.p, nq, fanout, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
+  if (c->timing) cudaEventRecord(c->ev[3], c->stream);
+  c->launches += 2;
+  search_units(c, d_q, nq, dim, c->unit_q.p, c->unit_p.p, nu, p, c->u_ids.p, c->u_dists.p, c->u_count.p, vis);
+  if (c->timing) cudaEventRecord(c->ev[4], c->stream);
+  cuda_check(dvsg::launch_combine(nq, fanout, c->u_ids.p, c->u_dists.p, c->u_count.p, p->k, p->k, d_ids, d_dists, d_count, c->err_flag.p, c->stream), "combine");
+  c->launches += 1;
+  if (d_vecs) {
+    build_locator(c);
+    cuda_check(dvsg::launch_gather_vectors(d_ids, d_count, nq, p->k, c->d_locator.p, c->vec.p, c->dim, c->dpad, d_vecs, c->stream), "gather vectors");
+    c->launches += 1;
+  }
+  if (c->timing) cudaEventRecord(c->ev[5], c->stream);
+}
+
+void check_err_flag(dvsg_ctx* c, const char* what) {
+  int flag = 0;
+  cuda_check(cudaMemcpyAsync(&flag, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "err flag");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  if (flag) fail(DVSG_EINTERNAL, "%s", what);
+}
+
+void read_timings(dvsg_ctx* c, bool pipeline) {
+  if (!c->timing) return;
+  cudaEventSynchronize(c->ev[pipeline ? 5 : 1]);
+  cudaEventElapsedTime(&c->t_search, c->ev[0], c->ev[1]);
+  if (pipeline) {
+    cudaEventElapsedTime(&c->t_assign, c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&c->t_combine, c->ev[4], c->ev[5]);
+    cudaEventElapsedTime(&c->t_total, c->ev[2], c->ev[5]);
+  } else {
+    c->t_assign = c->t_combine = 0;
+    c->t_total = c->t_search;
+  }
+}
+
+// ---- FNSY v1 (index_file.cpp:16-25) -------------------------------------
+struct Section {
+  uint32_t id;
+  uint64_t offset;  // payload offset in the file
+  uint64_t length;
+};
+
+struct FileReader {
+  FILE* f = nullptr;
+  uint64_t pos = 0;
+  explicit FileReader(const char* path) {
+    f = std::fopen(path, "rb");
+    if (!f) fail(DVSG_EFORMAT, "cannot open %s for reading (byte offset 0)", path);
+  }
+  ~FileReader() {
+    if (f) std::fclose(f);
+  }
+  void seek(uint64_t off) {
+    if (fseeko(f, (off_t)off, SEEK_SET) != 0) fail(DVSG_EFORMAT, "index file: seek failed (byte offset %llu)", (unsigned long long)off);
+    pos = off;
+  }
+  bool read(void* dst, size_t n) {
+    const size_t got = std::fread(dst, 1, n, f);
+    pos += got;
+    return got == n;
+  }
+};
+
+struct SecCursor {
+  FileReader& r;
+  const char* name;
+  uint64_t begin, end;
+  SecCursor(FileReader& rr, const Section& s, const char* nm) : r(rr), name(nm), begin(s.offset), end(s.offset + s.length) { r.seek(begin); }
+  uint64_t offset() const { return r.pos; }
+  void need(uint64_t bytes) {
+    if (r.pos + bytes > end) fail(DVSG_EFORMAT, "index file: truncated %s section (byte offset %llu)", name, (unsigned long long)r.pos);
+  }
+  uint32_t u32() {
+    need(4);
+    unsigned char b[4];
+    if (!r.read(b, 4)) fail(DVSG_EFORMAT, "index file: truncated %s section (byte offset %llu)", name, (unsigned long long)r.pos);
+    return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+  }
+  void bulk(void* dst, uint64_t bytes) {  // little-endian host assumed (x86-64)
+    need(bytes);
+    if (!r.read(dst, bytes)) fail(DVSG_EFORMAT, "index file: truncated %s section (byte offset %llu)", name, (unsigned long long)r.pos);
+  }
+  void skip(uint64_t bytes) {
+    need(bytes);
+    r.seek(r.pos + bytes);
+  }
+  void expect_consumed() {
+    if (r.pos != end) fail(DVSG_EFORMAT, "index file: trailing bytes in %s section (byte offset %llu)", name, (unsigned long long)r.pos);
+  }
+};
+
+void put_u32(std::vector<unsigned char>& b, uint32_t v) {
+  for (int i = 0; i < 4; ++i) b.push_back((unsigned char)((v >> (8 * i)) & 0xff));
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* dvsg_last_error(void) { return g_err.c_str(); }
+const char* dvsg_version(void) { return "dvsg 0.1 (sm_100a)"; }
+
+dvsg_status dvsg_create(int device, dvsg_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(DVSG_EINVAL, "dvsg_create: null out");
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) fail(DVSG_EINVAL, "dvsg_create: device %d out of range (%d devices)", device, n);
+    auto c = std::make_unique<dvsg_ctx>();
+    c->device = device;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, device), "props");
+    if (prop.major < 10) fail(DVSG_EINTERNAL, "dvsg: device %d is sm_%d%d; this library is built for sm_100a only", device, prop.major, prop.minor);
+    c->num_sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking), "stream");
+    for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
+    *out = c.release();
+  });
+}
+
+dvsg_status dvsg_destroy(dvsg_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->comm);
+    delete c;
+  });
+}
+
+void* dvsg_stream(dvsg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+dvsg_status dvsg_synchronize(dvsg_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+  });
+}
+
+dvsg_status dvsg_index_reset(dvsg_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    c->parts.clear();
+    c->rows = 0;
+    c->dim = c->dpad = c->dg = 0;
+    c->clusters = 0;
+    c->cents.clear();
+    c->placement.clear();
+    c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
+  });
+}
+
+dvsg_status dvsg_set_centroids(dvsg_ctx* c, const float* centroids, int clusters, int dim,
+                               const uint32_t* cluster_to_rank, int ranks) {
+  return guarded([&] {
+    set_device(c);
+    if (clusters < 1 || dim < 1 || !centroids) fail(DVSG_EINVAL, "assign_top_c: empty centroids");
+    if (c->dim && dim != c->dim) fail(DVSG_EINVAL, "set_centroids: dim %d != index dim %d", dim, c->dim);
+    if (ranks < 1) fail(DVSG_EINVAL, "ClusterTopology: ranks must be >= 1");
+    if (!finite_all(centroids, (uint64_t)clusters * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite centroid element");
+    c->clusters = clusters;
+    c->ranks = ranks;
+    c->cents.assign(centroids, centroids + (size_t)clusters * dim);
+    c->placement.resize((size_t)clusters);
+    for (int i = 0; i < clusters; ++i) {
+      const uint32_t r = cluster_to_rank ? cluster_to_rank[i] : (uint32_t)(i % ranks);  // router.cpp:38-41
+      if ((int)r >= ranks) fail(DVSG_EINVAL, "placement rank %u out of range", r);
+      c->placement[(size_t)i] = r;
+    }
+    std::vector<double> norms((size_t)clusters);
+    for (int j = 0; j < clusters; ++j) {  // refresh_center_norms, kmeans.cpp:34-40
+      double acc = 0.0;
+      for (int i = 0; i < dim; ++i) acc += (double)centroids[(size_t)j * dim + i] * (double)centroids[(size_t)j * dim + i];
+      norms[(size_t)j] = acc;
+    }
+    if (!c->dim) c->dim = dim;
+    c->d_cents.reserve((size_t)clusters * dim, c->stream);
+    c->d_cent_norms.reserve((size_t)clusters, c->stream);
+    cuda_check(cudaMemcpyAsync(c->d_cents.p, centroids, (size_t)clusters * dim * 4, cudaMemcpyHostToDevice, c->stream), "cents");
+    cuda_check(cudaMemcpyAsync(c->d_cent_norms.p, norms.data(), (size_t)clusters * 8, cudaMemcpyHostToDevice, c->stream), "norms");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    c->slot_dirty = true;
+  });
+}
+
+dvsg_status dvsg_load_partition(dvsg_ctx* c, uint32_t cluster, uint64_t n, int dim, int out_degree,
+                                const float* vectors, const uint32_t* adjacency,
+                                const uint32_t* global_ids, const uint32_t* entry_order) {
+  return guarded([&] {
+    set_device(c);
+    if (n == 0) fail(DVSG_EINVAL, "BuiltIndex: empty partition");
+    if (n >= (1ull << 31)) fail(DVSG_EINVAL, "load_partition: %llu rows exceed the 2^31 local-id limit", (unsigned long long)n);
+    if (dim < 1) fail(DVSG_EINVAL, "Dataset: dim must be positive, got %d", dim);
+    if (out_degree < 1) fail(DVSG_EINVAL, "build_graph: out_degree must be >= 1");
+    if (!vectors || !adjacency) fail(DVSG_EINVAL, "load_partition: null vectors/adjacency");
+    if (c->dim && c->dim != dim) fail(DVSG_EINVAL, "BuiltIndex: graph dim mismatch (%d vs %d)", dim, c->dim);
+    if (c->dg && c->dg != out_degree) fail(DVSG_EINVAL, "BuiltIndex: graph out-degree mismatch (%d vs %d)", out_degree, c->dg);
+    if (slot_of(c, cluster) >= 0) fail(DVSG_EINVAL, "load_partition: cluster %u already resident", cluster);
+    if (!finite_all(vectors, n * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite element in partition %u", cluster);
+    for (uint64_t i = 0; i < n * (uint64_t)out_degree; ++i)
+      if (adjacency[i] >= n) fail(DVSG_EFORMAT, "index file: neighbor id out of range in cluster %u", cluster);
+    std::vector<uint32_t> eo;
+    if (!entry_order) {
+      eo.resize(n);
+      entry_order_host(vectors, n, dim, eo.data());
+      entry_order = eo.data();
+    }
+    std::vector<uint32_t> iota;
+    if (!global_ids) {
+      iota.resize(n);
+      std::iota(iota.begin(), iota.end(), 0u);
+      global_ids = iota.data();
+    }
+    c->dim = dim;
+    c->dpad = (dim + 3) & ~3;
+    c->dg = out_degree;
+    const uint64_t r0 = c->rows, r1 = r0 + n;
+    c->vec.reserve(r1 * (uint64_t)c->dpad, c->stream, true, r0 * (uint64_t)c->dpad);
+    c->adj.reserve(r1 * (uint64_t)c->dg, c->stream, true, r0 * (uint64_t)c->dg);
+    c->gids.reserve(r1, c->stream, true, r0);
+    c->entry.reserve(r1, c->stream, true, r0);
+    if (c->dpad == dim) {
+      cuda_check(cudaMemcpy(c->vec.p + r0 * c->dpad, vectors, n * (uint64_t)dim * 4, cudaMemcpyHostToDevice), "vectors H2D");
+    } else {
+      cuda_check(cudaMemcpy2D(c->vec.p + r0 * c->dpad, (size_t)c->dpad * 4, vectors, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "vectors H2D");
+      cuda_check(cudaMemset2D(reinterpret_cast<char*>(c->vec.p + r0 * c->dpad) + (size_t)dim * 4, (size_t)c->dpad * 4, 0, (size_t)(c->dpad - dim) * 4, n), "pad");
+    }
+    cuda_check(cudaMemcpy(c->adj.p + r0 * c->dg, adjacency, n * (uint64_t)c->dg * 4, cudaMemcpyHostToDevice), "adjacency H2D");
+    cuda_check(cudaMemcpy(c->gids.p + r0, global_ids, n * 4, cudaMemcpyHostToDevice), "gids H2D");
+    cuda_check(cudaMemcpy(c->entry.p + r0, entry_order, n * 4, cudaMemcpyHostToDevice), "entry H2D");
+    c->parts.push_back(dvsg::PartDesc{r0, (uint32_t)n, cluster});
+    c->rows = r1;
+    c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
+  });
+}
+
+dvsg_status dvsg_index_info(dvsg_ctx* c, int* nparts, int* dim, int* out_degree, int* clusters,
+                            uint32_t* cluster_ids, uint64_t* sizes) {
+  return guarded([&] {
+    if (nparts) *nparts = (int)c->parts.size();
+    if (dim) *dim = c->dim;
+    if (out_degree) *out_degree = c->dg;
+    if (clusters) *clusters = c->clusters;
+    for (size_t i = 0; i < c->parts.size(); ++i) {
+      if (cluster_ids) cluster_ids[i] = c->parts[i].cluster;
+      if (sizes) sizes[i] = c->parts[i].n;
+    }
+  });
+}
+
+dvsg_status dvsg_get_entry_order(dvsg_ctx* c, uint32_t cluster, uint32_t* out) {
+  return guarded([&] {
+    set_device(c);
+    const int32_t s = slot_of(c, cluster);
+    if (s < 0) fail(DVSG_EINVAL, "cluster %u not resident", cluster);
+    const auto& pd = c->parts[(size_t)s];
+    cuda_check(cudaMemcpy(out, c->entry.p + pd.row_off, (size_t)pd.n * 4, cudaMemcpyDeviceToHost), "entry D2H");
+  });
+}
+
+dvsg_status dvsg_compute_entry_order(const float* vectors, uint64_t n, int dim, uint32_t* out) {
+  return guarded([&] {
+    if (n == 0 || dim < 1) fail(DVSG_EINVAL, "compute_entry_order: empty partition");
+    entry_order_host(vectors, n, dim, out);
+  });
+}
+
+dvsg_status dvsg_beam_search(dvsg_ctx* c, uint32_t cluster, const float* queries, uint64_t nq, int dim,
+                             const dvsg_search_params* p, uint32_t* out_ids, float* out_dists,
+                             uint32_t* out_count, uint64_t* out_visited) {
+  return guarded([&] {
+    set_device(c);
+    validate_params(p);
+    const int32_t slot = slot_of(c, cluster);
+    if (slot < 0) fail(DVSG_EINVAL, "beam_search: empty graph (cluster %u not resident)", cluster);
+    if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
+    if (nq == 0) return;
+    if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
+    const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
+    std::vector<uint32_t> uq(nq), up(nq, (uint32_t)slot);
+    std::iota(uq.begin(), uq.end(), 0u);
+    stage(c->unit_q, uq.data(), nq, c->stream);
+    stage(c->unit_p, up.data(), nq, c->stream);
+    const uint64_t k = (uint64_t)p->k;
+    c->u_ids.reserve(nq * k, c->stream);
+    c->u_dists.reserve(nq * k, c->stream);
+    c->u_count.reserve(nq, c->stream);
+    c->u_visited.reserve(nq, c->stream);
+    search_units(c, d_q, nq, dim, c->unit_q.p, c->unit_p.p, nq, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
+    cuda_check(cudaMemcpyAsync(out_ids, c->u_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_dists, c->u_dists.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_count, c->u_count.p, nq * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_visited, c->u_visited.p, nq * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "beam_search");
+    read_timings(c, false);
+  });
+}
+
+dvsg_status dvsg_search_units_device(dvsg_ctx* c, const float* d_queries, uint64_t nq, int dim,
+                                     const uint32_t* d_unit_query, const uint32_t* d_unit_cluster,
+                                     uint64_t nunits, const dvsg_search_params* p, uint32_t* d_out_ids,
+                                     float* d_out_dists, uint32_t* d_out_count, uint64_t* d_out_visited) {
+  return guarded([&] {
+    set_device(c);
+    // unit_cluster holds cluster ids: translate to resident slots on device
+    sync_slots(c);
+    c->unit_p.reserve(std::max<uint64_t>(nunits, 1), c->stream);
+    c->unit_q.reserve(std::max<uint64_t>(nunits, 1), c->stream);
+    c->err_flag.reserve(1, c->stream);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+    // route_kernel with fanout 1 maps cluster -> slot and writes unit_query = u;
+    // the caller's unit_query is then used directly.
+    cuda_check(dvsg::launch_route(d_unit_cluster, nunits, 1, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
+    c->launches += 1;
+    search_units(c, d_queries, nq, dim, d_unit_query, c->unit_p.p, nunits, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
+  });
+}
+
+dvsg_status dvsg_assign_top_c(dvsg_ctx* c, const float* queries, uint64_t nq, int dim, int cc, uint32_t* out) {
+  return guarded([&] {
+    set_device(c);
+    if (c->clusters < 1) fail(DVSG_EINVAL, "assign_top_c: empty centroids");
+    if (cc < 1 || cc > c->clusters) fail(DVSG_EINVAL, "assign_top_c: c=%d out of range for %d clusters", cc, c->clusters);
+    if (dim != c->dim) fail(DVSG_EINVAL, "assign_top_c: query dim %d != centroid dim %d", dim, c->dim);
+    if (nq == 0) return;
+    if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
+    const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
+    c->assign.reserve(nq * (uint64_t)cc, c->stream);
+    cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, c->assign.p, c->stream), "assign");
+    c->launches += 1;
+    cuda_check(cudaMemcpyAsync(out, c->assign.p, nq * (uint64_t)cc * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "assign");
+  });
+}
+
+dvsg_status dvsg_combine_results(dvsg_ctx* c, uint64_t nq, int nparts, const uint32_t* ids,
+                                 const float* dists, const uint32_t* counts, int stride, int k,
+                                 uint32_t* out_ids, float* out_dists, uint32_t* out_count) {
+  return guarded([&] {
+    set_device(c);
+    if (k < 1) fail(DVSG_EINVAL, "combine_results: k must be >= 1");
+    if (nparts < 0 || nparts > 32) fail(DVSG_EINVAL, "combine_results: %d partials above the device merge width 32", nparts);
+    if (stride < 0) fail(DVSG_EINVAL, "combine_results: negative stride");
+    for (uint64_t i = 0; i < nq * (uint64_t)nparts; ++i)
+      if ((int64_t)counts[i] > stride) fail(DVSG_EINVAL, "combine_results: partial count %u above stride %d", counts[i], stride);
+    if (nq == 0) return;
+    if (nparts == 0) {
+      for (uint64_t q = 0; q < nq; ++q) out_count[q] = 0;
+      return;
+    }
+    const uint64_t tot = nq * (uint64_t)nparts * (uint64_t)stride;
+    DevBuf<uint32_t> di, dc, oi, oc;
+    DevBuf<float> dd, od;
+    stage(di, ids, tot, c->stream);
+    stage(dd, dists, tot, c->stream);
+    stage(dc, counts, nq * (uint64_t)nparts, c->stream);
+    oi.reserve(nq * (uint64_t)k, c->stream);
+    od.reserve(nq * (uint64_t)k, c->stream);
+    oc.reserve(nq, c->stream);
+    c->err_flag.reserve(1, c->stream);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+    cuda_check(dvsg::launch_combine(nq, nparts, di.p, dd.p, dc.p, stride, k, oi.p, od.p, oc.p, c->err_flag.p, c->stream), "combine");
+    c->launches += 1;
+    check_err_flag(c, "combine_results: partial list not sorted by (dist, id)");
+    cuda_check(cudaMemcpy(out_ids, oi.p, nq * (uint64_t)k * 4, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(out_dists, od.p, nq * (uint64_t)k * 4, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(out_count, oc.p, nq * 4, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, int dim,
+                              const dvsg_search_params* p, int fanout, int ranks, int batch_index,
+                              uint32_t* out_ids, float* out_dists, uint32_t* out_count,
+                              float* out_vectors, uint64_t* visited_total) {
+  return guarded([&] {
+    set_device(c);
+    validate_params(p);
+    // simulator.cpp:250-273 validation order
+    if (c->clusters < 1 || c->parts.empty()) fail(DVSG_EINVAL, "BuiltIndex: index is not built");
+    if ((int)c->parts.size() != c->clusters) fail(DVSG_EINVAL, "BuiltIndex: %zu graphs for %d clusters", c->parts.size(), c->clusters);
+    if (dim != c->dim) fail(DVSG_EINVAL, "run_pipeline: query dim %d != index dim %d", dim, c->dim);
+    if (fanout < 1 || fanout > c->clusters) fail(DVSG_EINVAL, "run_pipeline: fanout %d out of range for %d clusters", fanout, c->clusters);
+    if (ranks != c->ranks) fail(DVSG_EINVAL, "run_pipeline: placement built for %d ranks, topology has %d", c->ranks, ranks);
+    if (nq < 2) fail(DVSG_EINVAL, "run_pipeline: two_microbatch mode needs >= 2 queries");
+    if (batch_index < 0) fail(DVSG_EINVAL, "origin_rank_for_batch: negative batch index");
+    if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
+    const uint64_t k = (uint64_t)p->k;
+    const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
+    c->io_u.reserve(nq * k + nq, c->stream);
+    DevBuf<float> od, ov;
+    od.reserve(nq * k, c->stream);
+    if (out_vectors) ov.reserve(nq * k * (uint64_t)dim, c->stream);
+    c->u_visited.reserve(nq * (uint64_t)fanout, c->stream);
+    if (out_vectors) build_locator(c);
+    pipeline_device(c, d_q, nq, dim, p, fanout, c->io_u.p, od.p, c->io_u.p + nq * k, out_vectors ? ov.p : nullptr, c->u_visited.p);
+    c->io_u64.reserve(1, c->stream);
+    cuda_check(dvsg::launch_reduce_u64(c->u_visited.p, nq * (uint64_t)fanout, reinterpret_cast<unsigned long long*>(c->io_u64.p), c->stream), "reduce");
+    c->launches += 1;
+    check_err_flag(c, "route: cluster id outside placement / not resident, or combine_results: partial list not sorted");
+    cuda_check(cudaMemcpy(out_ids, c->io_u.p, nq * k * 4, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(out_dists, od.p, nq * k * 4, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(out_count, c->io_u.p + nq * k, nq * 4, cudaMemcpyDeviceToHost), "D2H");
+    if (out_vectors) cuda_check(cudaMemcpy(out_vectors, ov.p, nq * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost), "D2H");
+    if (visited_total) cuda_check(cudaMemcpy(visited_total, c->io_u64.p, 8, cudaMemcpyDeviceToHost), "D2H");
+    read_timings(c, true);
+  });
+}
+
+dvsg_status dvsg_run_pipeline_device(dvsg_ctx* c, const float* d_queries, uint64_t nq, int dim,
+                                     const dvsg_search_params* p, int fanout, uint32_t* d_out_ids,
+                                     float* d_out_dists, uint32_t* d_out_count, float* d_out_vectors,
+                                     uint64_t* d_visited) {
+  return guarded([&] {
+    set_device(c);
+    if (d_out_vectors) build_locator(c);
+    pipeline_device(c, d_queries, nq, dim, p, fanout, d_out_ids, d_out_dists, d_out_count, d_out_vectors, d_visited);
+  });
+}
+
+dvsg_status dvsg_build_graph(dvsg_ctx* c, const float* vectors, uint64_t n, int dim, int out_degree,
+                             uint32_t* adjacency_out) {
+  return guarded([&] {
+    set_device(c);
+    if (n == 0) fail(DVSG_EINVAL, "build_graph: empty partition");
+    if (out_degree < 1) fail(DVSG_EINVAL, "build_graph: out_degree must be >= 1");
+    if (out_degree > 32) fail(DVSG_EINVAL, "build_graph: out_degree %d above the device limit 32", out_degree);
+    if (dim < 1) fail(DVSG_EINVAL, "Dataset: dim must be positive, got %d", dim);
+    if (!finite_all(vectors, n * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite element");
+    const int dpad = (dim + 3) & ~3;
+    DevBuf<float> dv;
+    DevBuf<uint32_t> da;
+    dv.reserve(n * (uint64_t)dpad, c->stream);
+    da.reserve(n * (uint64_t)out_degree, c->stream);
+    cuda_check(cudaMemset(dv.p, 0, n * (uint64_t)dpad * 4), "memset");
+    cuda_check(cudaMemcpy2D(dv.p, (size_t)dpad * 4, vectors, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(dvsg::launch_knn_build(dv.p, n, dim, dpad, out_degree, da.p, c->stream), "knn build");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "knn build");
+    cuda_check(cudaMemcpy(adjacency_out, da.p, n * (uint64_t)out_degree * 4, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+dvsg_status dvsg_set_timing(dvsg_ctx* c, int enabled) {
+  return guarded([&] { c->timing = enabled != 0; });
+}
+
+dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, float* combine_ms, float* total_ms) {
+  return guarded([&] {
+    if (search_ms) *search_ms = c->t_search;
+    if (assign_ms) *assign_ms = c->t_assign;
+    if (combine_ms) *combine_ms = c->t_combine;
+    if (total_ms) *total_ms = c->t_total;
+  });
+}
+
+uint64_t dvsg_kernel_launches(dvsg_ctx* c) { return c ? c->launches.load() : 0; }
+
+// ---- FNSY v1 -------------------------------------------------------------
+dvsg_status dvsg_load_index_file(dvsg_ctx* c, const char* path, int rank) {
+  return guarded([&] {
+    set_device(c);
+    FileReader r(path);
+    char magic[4];
+    if (!r.read(magic, 4) || std::memcmp(magic, "FNSY", 4) != 0) fail(DVSG_EFORMAT, "index file: bad magic (expected FNSY) (byte offset 0)");
+    unsigned char vb[4];
+    if (!r.read(vb, 4) || ((uint32_t)vb[0] | ((uint32_t)vb[1] << 8) | ((uint32_t)vb[2] << 16) | ((uint32_t)vb[3] << 24)) != 1u)
+      fail(DVSG_EFORMAT, "index file: unsupported version (byte offset 4)");
+    // scan section headers (index_file.cpp:164-195)
+    Section secs[6] = {};
+    bool have[6] = {};
+    static const char* names[6] = {"", "centroids", "placement", "global ids", "adjacency", "vectors"};
+    uint64_t off = 8;
+    for (;;) {
+      unsigned char h[12];
+      const size_t got = std::fread(h, 1, 12, r.f);
+      if (got == 0) break;
+      if (got < 4) fail(DVSG_EFORMAT, "index file: truncated section header (byte offset %llu)", (unsigned long long)off);
+      if (got < 12) fail(DVSG_EFORMAT, "index file: truncated section length (byte offset %llu)", (unsigned long long)(off + 4));
+      uint32_t id = (uint32_t)h[0] | ((uint32_t)h[1] << 8) | ((uint32_t)h[2] << 16) | ((uint32_t)h[3] << 24);
+      uint64_t len = 0;
+      for (int i = 0; i < 8; ++i) len |= (uint64_t)h[4 + i] << (8 * i);
+      if (id < 1 || id > 5) fail(DVSG_EFORMAT, "index file: unknown section id %u (byte offset %llu)", id, (unsigned long long)off);
+      if (have[id]) fail(DVSG_EFORMAT, "index file: duplicate %s section (byte offset %llu)", names[id], (unsigned long long)off);
+      if (fseeko(r.f, 0, SEEK_END) != 0) fail(DVSG_EFORMAT, "index file: seek failed");
+      const uint64_t fsize = (uint64_t)ftello(r.f);
+      if (off + 12 + len > fsize) fail(DVSG_EFORMAT, "index file: truncated section payload (byte offset %llu)", (unsigned long long)(off + 12));
+      have[id] = true;
+      secs[id] = Section{id, off + 12, len};
+      off += 12 + len;
+      r.seek(off);
+    }
+    for (uint32_t id = 1; id <= 5; ++id)
+      if (!have[id]) fail(DVSG_EFORMAT, "index file: missing section id %u (byte offset %llu)", id, (unsigned long long)off);
+
+    SecCursor cent(r, secs[1], names[1]);
+    const uint32_t clusters = cent.u32();
+    const uint32_t dim = cent.u32();
+    if (clusters == 0 || dim == 0) fail(DVSG_EFORMAT, "index file: empty centroids section (byte offset %llu)", (unsigned long long)cent.offset());
+    std::vector<float> centroids((size_t)clusters * dim);
+    cent.bulk(centroids.data(), centroids.size() * 4);
+    cent.expect_consumed();
+
+    SecCursor plac(r, secs[2], names[2]);
+    if (plac.u32() != clusters) fail(DVSG_EFORMAT, "index file: placement cluster count mismatch (byte offset %llu)", (unsigned long long)plac.offset());
+    const uint32_t ranks = plac.u32();
+    std::vector<uint32_t> placement(clusters);
+    for (auto& x : placement) {
+      x = plac.u32();
+      if (x >= ranks) fail(DVSG_EFORMAT, "index file: placement rank out of range (byte offset %llu)", (unsigned long long)plac.offset());
+    }
+    plac.expect_consumed();
+
+    SecCursor gid(r, secs[3], names[3]);
+    if (gid.u32() != clusters) fail(DVSG_EFORMAT, "index file: global id cluster count mismatch (byte offset %llu)", (unsigned long long)gid.offset());
+    std::vector<uint64_t> gid_off(clusters), sizes(clusters);
+    for (uint32_t cl = 0; cl < clusters; ++cl) {
+      sizes[cl] = gid.u32();
+      gid_off[cl] = gid.offset();
+      gid.skip(sizes[cl] * 4);
+    }
+    gid.expect_consumed();
+
+    SecCursor adj(r, secs[4], names[4]);
+    if (adj.u32() != clusters) fail(DVSG_EFORMAT, "index file: adjacency cluster count mismatch (byte offset %llu)", (unsigned long long)adj.offset());
+    const uint32_t dg = adj.u32();
+    if ((int32_t)dg < 1) fail(DVSG_EFORMAT, "index file: non-positive out-degree (byte offset %llu)", (unsigned long long)adj.offset());
+    std::vector<uint64_t> adj_off(clusters);
+    for (uint32_t cl = 0; cl < clusters; ++cl) {
+      const uint32_t cnt = adj.u32();
+      if (cnt != sizes[cl]) fail(DVSG_EFORMAT, "index file: adjacency node count mismatch in cluster %u (byte offset %llu)", cl, (unsigned long long)adj.offset());
+      adj_off[cl] = adj.offset();
+      adj.skip((uint64_t)cnt * dg * 4);
+    }
+    adj.expect_consumed();
+
+    SecCursor vs(r, secs[5], names[5]);
+    if (vs.u32() != clusters) fail(DVSG_EFORMAT, "index file: vector cluster count mismatch (byte offset %llu)", (unsigned long long)vs.offset());
+    if (vs.u32() != dim) fail(DVSG_EFORMAT, "index file: vector dim mismatch (byte offset %llu)", (unsigned long long)vs.offset());
+    std::vector<uint64_t> vec_off(clusters);
+    for (uint32_t cl = 0; cl < clusters; ++cl) {
+      const uint32_t cnt = vs.u32();
+      if (cnt != sizes[cl]) fail(DVSG_EFORMAT, "index file: vector node count mismatch in cluster %u (byte offset %llu)", cl, (unsigned long long)vs.offset());
+      vec_off[cl] = vs.offset();
+      vs.skip((uint64_t)cnt * dim * 4);
+    }
+    vs.expect_consumed();
+    for (uint32_t cl = 0; cl < clusters; ++cl)
+      if (sizes[cl] == 0) fail(DVSG_EINVAL, "BuiltIndex: empty partition");
+
+    // all structural checks passed: reset and upload the owned partitions
+    c->parts.clear();
+    c->rows = 0;
+    c->dim = c->dpad = c->dg = 0;
+    c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
+    std::vector<float> v;
+    std::vector<uint32_t> a, g;
+    for (uint32_t cl = 0; cl < clusters; ++cl) {
+      if (rank >= 0 && placement[cl] != (uint32_t)rank) continue;
+      const uint64_t n = sizes[cl];
+      v.resize(n * dim);
+      a.resize(n * dg);
+      g.resize(n);
+      r.seek(gid_off[cl]);
+      if (!r.read(g.data(), n * 4)) fail(DVSG_EFORMAT, "index file: truncated global ids section");
+      r.seek(adj_off[cl]);
+      if (!r.read(a.data(), n * dg * 4)) fail(DVSG_EFORMAT, "index file: truncated adjacency section");
+      for (uint64_t i = 0; i < n * dg; ++i)
+        if (a[i] >= n) fail(DVSG_EFORMAT, "index file: neighbor id out of range in cluster %u (byte offset %llu)", cl, (unsigned long long)(adj_off[cl] + 4 * i));
+      r.seek(vec_off[cl]);
+      if (!r.read(v.data(), n * dim * 4)) fail(DVSG_EFORMAT, "index file: truncated vectors section");
+      const dvsg_status st = dvsg_load_partition(c, cl, n, (int)dim, (int)dg, v.data(), a.data(), g.data(), nullptr);
+      if (st != DVSG_OK) fail(st, "%s", g_err.c_str());
+    }
+    const dvsg_status st = dvsg_set_centroids(c, centroids.data(), (int)clusters, (int)dim, placement.data(), (int)ranks);
+    if (st != DVSG_OK) fail(st, "%s", g_err.c_str());
+  });
+}
+
+dvsg_status dvsg_save_index_file(const char* path, int clusters, int dim, int out_degree,
+                                 const float* centroids, const uint32_t* cluster_to_rank, int ranks,
+                                 const uint64_t* offsets, const float* vectors,
+                                 const uint32_t* adjacency, const uint32_t* global_ids) {
+  return guarded([&] {
+    if (clusters < 1 || dim < 1 || out_degree < 1 || ranks < 1) fail(DVSG_EINVAL, "BuiltIndex: index is not built");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(DVSG_EFORMAT, "cannot open %s for writing (byte offset 0)", path);
+    std::unique_ptr<FILE, int (*)(FILE*)> guard(f, std::fclose);
+    auto w = [&](const void* p, size_t n) {
+      if (n && std::fwrite(p, 1, n, f) != n) fail(DVSG_EFORMAT, "write failure on %s (byte offset 0)", path);
+    };
+    auto section = [&](uint32_t id, const std::vector<unsigned char>& head, const std::vector<std::pair<const void*, uint64_t>>& bulk) {
+      uint64_t len = head.size();
+      for (auto& b : bulk) len += b.second;
+      std::vector<unsigned char> h;
+      put_u32(h, id);
+      put_u32(h, (uint32_t)(len & 0xffffffffu));
+      put_u32(h, (uint32_t)(len >> 32));
+      w(h.data(), h.size());
+      w(head.data(), head.size());
+      for (auto& b : bulk) w(b.first, b.second);
+    };
+    w("FNSY", 4);
+    std::vector<unsigned char> v;
+    put_u32(v, 1);
+    w(v.data(), 4);
+    const uint32_t C = (uint32_t)clusters;
+    std::vector<unsigned char> h;
+    put_u32(h, C);
+    put_u32(h, (uint32_t)dim);
+    section(1, h, {{centroids, (uint64_t)C * dim * 4}});
+    h.clear();
+    put_u32(h, C);
+    put_u32(h, (uint32_t)ranks);
+    std::vector<uint32_t> plc(C);
+    for (uint32_t i = 0; i < C; ++i) plc[i] = cluster_to_rank ? cluster_to_rank[i] : i % (uint32_t)ranks;
+    section(2, h, {{plc.data(), (uint64_t)C * 4}});
+    // per-cluster sections interleave a u32 count before each payload
+    std::vector<std::vector<unsigned char>> counts(C);
+    std::vector<std::pair<const void*, uint64_t>> bulk;
+    for (uint32_t cl = 0; cl < C; ++cl) {
+      put_u32(counts[cl], (uint32_t)(offsets[cl + 1] - offsets[cl]));
+    }
+    h.clear();
+    put_u32(h, C);
+    bulk.clear();
+    for (uint32_t cl = 0; cl < C; ++cl) {
+      bulk.push_back({counts[cl].data(), 4});
+      bulk.push_back({global_ids + offsets[cl], (offsets[cl + 1] - offsets[cl]) * 4});
+    }
+    section(3, h, bulk);
+    h.clear();
+    put_u32(h, C);
+    put_u32(h, (uint32_t)out_degree);
+    bulk.clear();
+    for (uint32_t cl = 0; cl < C; ++cl) {
+      bulk.push_back({counts[cl].data(), 4});
+      bulk.push_back({adjacency + offsets[cl] * (uint64_t)out_degree, (offsets[cl + 1] - offsets[cl]) * (uint64_t)out_degree * 4});
+    }
+    section(4, h, bulk);
+    h.clear();
+    put_u32(h, C);
+    put_u32(h, (uint32_t)dim);
+    bulk.clear();
+    for (uint32_t cl = 0; cl < C; ++cl) {
+      bulk.push_back({counts[cl].data(), 4});
+      bulk.push_back({vectors + offsets[cl] * (uint64_t)dim, (offsets[cl + 1] - offsets[cl]) * (uint64_t)dim * 4});
+    }
+    section(5, h, bulk);
+    if (std::fflush(f) != 0) fail(DVSG_EFORMAT, "write failure on %s (byte offset 0)", path);
+  });
+}
+
+}  // extern "C"

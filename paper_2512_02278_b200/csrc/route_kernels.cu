@@ -1,0 +1,231 @@
+// route_kernels.cu -- K5 assign, route, K4 combine, hit-vector gather.
+//
+//   K5 assign   : assign_top_c, /root/reference/proj/src/kmeans.cpp:243-280.
+//                 One warp per query; each lane owns whole centroids and runs
+//                 the reference's own sequential fp64 dot / norm (kmeans.cpp
+//                 :44-48 expanded_dist), so the f32 distances are bit-exact.
+//   route       : router.cpp:52-79 -- one unit per (query, assigned cluster).
+//   K4 combine  : combine_results, simulator.cpp:219-243.  One warp per query
+//                 runs a <=32-way merge of the sorted partial lists on
+//                 (dist, id) keys, dedups by id, truncates at k, and flags an
+//                 unsorted partial (internal_error in the reference).
+//   gather      : simulator.cpp:329-333 -- attach the hit vectors.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dvsg_internal.h"
+
+namespace dvsg {
+namespace {
+
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  if (f == 0.0f) f = 0.0f;
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  const uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(u);
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// scratch: nq x clusters keys (ord(dist) << 32 | cluster)
+__global__ void assign_kernel(const float* __restrict__ queries, uint64_t nq, int dim,
+                              const float* __restrict__ cents,
+                              const double* __restrict__ cent_norms, int clusters, int c,
+                              uint64_t* __restrict__ scratch, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t q = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const float* qp = queries + q * (uint64_t)dim;
+  double qn = 0.0;  // squared_norm, distance.cpp:44-50 (sequential)
+  for (int i = 0; i < dim; ++i) qn = __dadd_rn(qn, __dmul_rn((double)qp[i], (double)qp[i]));
+  uint64_t* row = scratch + q * (uint64_t)clusters;
+  for (int j = lane; j < clusters; j += 32) {
+    const float* cp = cents + (uint64_t)j * (uint64_t)dim;
+    double dot = 0.0;  // dot, distance.cpp:35-42 (sequential)
+    for (int i = 0; i < dim; ++i) dot = __dadd_rn(dot, __dmul_rn((double)qp[i], (double)cp[i]));
+    const double d = __dsub_rn(__dadd_rn(qn, cent_norms[j]), __dmul_rn(2.0, dot));
+    const float f = (float)(d < 0.0 ? 0.0 : d);
+    row[j] = ((uint64_t)f2ord(f) << 32) | (uint32_t)j;
+  }
+  __syncwarp();
+  // c rounds of warp-min over keys strictly above the last selected one
+  uint64_t last = 0;
+  for (int r = 0; r < c; ++r) {
+    uint64_t best = ~0ull;
+    for (int j = lane; j < clusters; j += 32) {
+      const uint64_t key = row[j];
+      if ((r == 0 || key > last) && key < best) best = key;
+    }
+    best = warp_min_u64(best);
+    if (lane == 0) out[q * (uint64_t)c + r] = (uint32_t)best;
+    last = best;
+  }
+}
+
+__global__ void route_kernel(const uint32_t* __restrict__ assign, uint64_t nq, int fanout,
+                             const int32_t* __restrict__ cluster_to_slot,
+                             uint32_t* __restrict__ unit_query, uint32_t* __restrict__ unit_part,
+                             int* err) {
+  const uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nq * (uint64_t)fanout) return;
+  const int32_t slot = cluster_to_slot[assign[u]];
+  if (slot < 0) {
+    atomicExch(err, 1);
+    unit_part[u] = 0;
+  } else {
+    unit_part[u] = (uint32_t)slot;
+  }
+  unit_query[u] = (uint32_t)(u / (uint64_t)fanout);
+}
+
+__global__ void combine_kernel(uint64_t nq, int nparts, const uint32_t* __restrict__ ids,
+                               const float* __restrict__ dists,
+                               const uint32_t* __restrict__ counts, int stride, int k,
+                               uint32_t* __restrict__ out_ids, float* __restrict__ out_dists,
+                               uint32_t* __restrict__ out_count, int* err) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t q = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const uint64_t base = q * (uint64_t)nparts;
+  // lane j < nparts owns partial list j
+  uint32_t cnt = 0, head = 0;
+  const uint32_t* li = nullptr;
+  const float* ld = nullptr;
+  if (lane < nparts) {
+    cnt = counts[base + lane];
+    li = ids + (base + lane) * (uint64_t)stride;
+    ld = dists + (base + lane) * (uint64_t)stride;
+    for (uint32_t i = 1; i < cnt; ++i) {
+      const uint64_t a = ((uint64_t)f2ord(ld[i - 1]) << 32) | li[i - 1];
+      const uint64_t b = ((uint64_t)f2ord(ld[i]) << 32) | li[i];
+      if (b < a) atomicExch(err, 1);  // "partial list not sorted by (dist, id)"
+    }
+  }
+  uint32_t* oi = out_ids + q * (uint64_t)k;
+  float* od = out_dists + q * (uint64_t)k;
+  int outn = 0;
+  for (;;) {
+    const uint64_t mine = head < cnt ? (((uint64_t)f2ord(ld[head]) << 32) | li[head]) : ~0ull;
+    const uint64_t best = warp_min_u64(mine);
+    if (best == ~0ull || outn >= k) break;
+    // unique winner (keys unique across lanes unless equal (dist,id) pairs)
+    const unsigned who = __ballot_sync(0xFFFFFFFFu, mine == best);
+    const int src = __ffs(who) - 1;
+    if (lane == src) ++head;
+    const uint32_t id = (uint32_t)best;
+    bool dup = false;
+    for (int i = lane; i < outn; i += 32) dup |= (oi[i] == id);
+    dup = __any_sync(0xFFFFFFFFu, dup);
+    if (!dup) {
+      if (lane == 0) {
+        oi[outn] = id;
+        od[outn] = ord2f((uint32_t)(best >> 32));
+      }
+      ++outn;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) out_count[q] = (uint32_t)outn;
+}
+
+__global__ void gather_vectors_kernel(const uint32_t* __restrict__ ids,
+                                      const uint32_t* __restrict__ counts, uint64_t nq, int k,
+                                      const uint64_t* __restrict__ locator,
+                                      const float* __restrict__ vectors, int dim, int dpad,
+                                      float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t slot = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (slot >= nq * (uint64_t)k) return;
+  const uint64_t q = slot / (uint64_t)k;
+  const uint32_t h = (uint32_t)(slot - q * (uint64_t)k);
+  if (h >= counts[q]) return;
+  const uint64_t row = locator[ids[slot]];
+  const float* src = vectors + row * (uint64_t)dpad;
+  float* dst = out + slot * (uint64_t)dim;
+  for (int i = lane; i < dim; i += 32) dst[i] = src[i];
+}
+
+__global__ void reduce_u64_kernel(const uint64_t* __restrict__ in, uint64_t n,
+                                  unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    acc += in[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+}  // namespace
+
+cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const float* cents,
+                          const double* cent_norms, int clusters, int c, uint32_t* out,
+                          cudaStream_t stream) {
+  if (nq == 0) return cudaSuccess;
+  uint64_t* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, sizeof(uint64_t) * nq * (uint64_t)clusters, stream);
+  if (e != cudaSuccess) return e;
+  const int wpb = 4;
+  assign_kernel<<<(unsigned)((nq + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
+      queries, nq, dim, cents, cent_norms, clusters, c, scratch, out);
+  e = cudaGetLastError();
+  cudaFreeAsync(scratch, stream);
+  return e;
+}
+
+cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,
+                         const int32_t* cluster_to_slot, uint32_t* unit_query,
+                         uint32_t* unit_part, int* err_flag, cudaStream_t stream) {
+  const uint64_t n = nq * (uint64_t)fanout;
+  if (n == 0) return cudaSuccess;
+  route_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(assign, nq, fanout,
+                                                                 cluster_to_slot, unit_query,
+                                                                 unit_part, err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(uint64_t nq, int nparts, const uint32_t* ids, const float* dists,
+                           const uint32_t* counts, int stride, int k, uint32_t* out_ids,
+                           float* out_dists, uint32_t* out_count, int* err_flag,
+                           cudaStream_t stream) {
+  if (nq == 0) return cudaSuccess;
+  if (nparts < 1 || nparts > 32) return cudaErrorInvalidValue;
+  const int wpb = 8;
+  combine_kernel<<<(unsigned)((nq + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
+      nq, nparts, ids, dists, counts, stride, k, out_ids, out_dists, out_count, err_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_vectors(const uint32_t* ids, const uint32_t* counts, uint64_t nq,
+                                  int k, const uint64_t* locator, const float* vectors,
+                                  int dim, int dpad, float* out, cudaStream_t stream) {
+  const uint64_t n = nq * (uint64_t)k;
+  if (n == 0) return cudaSuccess;
+  const int wpb = 8;
+  gather_vectors_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
+      ids, counts, nq, k, locator, vectors, dim, dpad, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_u64(const uint64_t* in, uint64_t n, unsigned long long* out,
+                              cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess || n == 0) return e;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  reduce_u64_kernel<<<(unsigned)blocks, 256, 0, stream>>>(in, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dvsg

@@ -1,0 +1,456 @@
+// search_kernel.cu -- K1: persistent batched greedy beam search for sm_100a.
+//
+// Semantics: beam_search_stats, /root/reference/proj/src/graph_index.cpp:105-187
+// (exact visited set, pool cap = max(4k, 2*I*w), frontier = first w
+// unexpanded pool entries, pool order (dist, local id), final order
+// (dist, global id), visited = number of vectors scored).
+//
+// Design (one CTA of 256 threads per (query, partition) unit, persistent
+// over a global work counter):
+//   * pool      : sorted u64 keys in smem, key = ord(dist)<<32 | local<<1 | expanded
+//                 (the expanded flag rides in bit 0, which never decides an
+//                 order because local ids are unique) -- double buffered.
+//   * visited   : exact open-addressing u32 hash, smem when it fits, else a
+//                 per-CTA region in global memory (L2-resident); never forgets,
+//                 like the reference's unordered_set (graph_index.cpp:133,165).
+//   * per chunk of <= 2048 raw candidate ids (entry nodes, or the adjacency
+//     rows of the frontier):
+//       dedup      -> warp-aggregated append of new ids (visited += new)
+//       score      -> one warp per vector, float4 gathers, U vectors in flight
+//                     per warp, fp64 (parity) or fp32 (fast) lane partials and
+//                     a butterfly tree
+//       filter     -> exact: drop keys above the current cap-th pool key
+//                     (they could not survive shrink())
+//       sort/merge -> bitonic sort of survivors, co-rank merge into the pool,
+//                     truncated at cap (== the reference's sort + resize)
+//   Chunking is exact because top-cap(A u B u C) = top-cap(top-cap(A u B) u C)
+//   for unique keys, and frontier selection only happens between iterations.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dvsg_internal.h"
+
+namespace dvsg {
+namespace {
+
+constexpr int kRawPerThread = kChunk / kThreads;  // 8
+
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  if (f == 0.0f) f = 0.0f;  // -0.0 == +0.0 in the reference's comparisons
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  const uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(u);
+}
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t id) { return id * 0x9E3779B1u; }
+
+// Exact insert; returns true when `id` was not present.
+__device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uint32_t id) {
+  uint32_t h = (hash_slot(id) >> 7) & mask;
+  for (;;) {
+    uint32_t cur = table[h];
+    if (cur == id) return false;
+    if (cur == kEmpty) {
+      cur = atomicCAS(table + h, kEmpty, id);
+      if (cur == kEmpty) return true;
+      if (cur == id) return false;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// number of elements of sorted arr[0..len) strictly below key
+__device__ __forceinline__ int lower_rank(const uint64_t* arr, int len, uint64_t key) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (arr[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Block-wide ascending bitonic sort of s[0..n), n a power of two.
+__device__ void bitonic_sort(uint64_t* s, int n) {
+  const int tid = threadIdx.x;
+  for (int kk = 2; kk <= n; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n; i += kThreads) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t x = s[i], y = s[ixj];
+          const bool up = (i & kk) == 0;
+          if ((x > y) == up) {
+            s[i] = y;
+            s[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int pow2_ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+template <typename ACC>
+__device__ __forceinline__ ACC warp_sum(ACC v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+template <typename ACC, int METRIC>
+__device__ __forceinline__ ACC lane_partial(const float4& x, const float4& q);
+
+template <>
+__device__ __forceinline__ double lane_partial<double, 0>(const float4& x, const float4& q) {
+  // sequential within the lane, no contraction: (x-q)^2 rounded then added
+  const double d0 = (double)x.x - (double)q.x, d1 = (double)x.y - (double)q.y;
+  const double d2 = (double)x.z - (double)q.z, d3 = (double)x.w - (double)q.w;
+  double acc = __dmul_rn(d0, d0);
+  acc = __dadd_rn(acc, __dmul_rn(d1, d1));
+  acc = __dadd_rn(acc, __dmul_rn(d2, d2));
+  acc = __dadd_rn(acc, __dmul_rn(d3, d3));
+  return acc;
+}
+template <>
+__device__ __forceinline__ double lane_partial<double, 1>(const float4& x, const float4& q) {
+  double acc = __dmul_rn((double)x.x, (double)q.x);
+  acc = __dadd_rn(acc, __dmul_rn((double)x.y, (double)q.y));
+  acc = __dadd_rn(acc, __dmul_rn((double)x.z, (double)q.z));
+  acc = __dadd_rn(acc, __dmul_rn((double)x.w, (double)q.w));
+  return acc;
+}
+template <>
+__device__ __forceinline__ float lane_partial<float, 0>(const float4& x, const float4& q) {
+  const float d0 = x.x - q.x, d1 = x.y - q.y, d2 = x.z - q.z, d3 = x.w - q.w;
+  float acc = d0 * d0;
+  acc = fmaf(d1, d1, acc);
+  acc = fmaf(d2, d2, acc);
+  acc = fmaf(d3, d3, acc);
+  return acc;
+}
+template <>
+__device__ __forceinline__ float lane_partial<float, 1>(const float4& x, const float4& q) {
+  float acc = x.x * q.x;
+  acc = fmaf(x.y, q.y, acc);
+  acc = fmaf(x.z, q.z, acc);
+  acc = fmaf(x.w, q.w, acc);
+  return acc;
+}
+
+__device__ __forceinline__ float4 ldg_f4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+struct BlockState {
+  uint64_t unit;
+  int ncand;
+  int nsurv;
+  int nf;
+  int warp_cnt[kWarps];
+};
+
+// VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
+template <int VPL, typename ACC, int METRIC>
+__global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a) {
+  constexpr int U = VPL >= 8 ? 1 : (8 / VPL);
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ BlockState st;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t* pool = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* pool_alt = pool + a.cap;
+  uint64_t* surv = pool_alt + a.cap;
+  uint32_t* cand = reinterpret_cast<uint32_t*>(surv + a.chp);
+  uint32_t* frontier = cand + kChunk;
+  uint32_t* table = a.hash_global ? a.hash_global + (size_t)blockIdx.x * (size_t)a.hsize
+                                  : frontier + ((a.beam + 3) & ~3);
+  const uint32_t hmask = (uint32_t)a.hsize - 1u;
+  const unsigned full = 0xFFFFFFFFu;
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  for (;;) {
+    if (tid == 0) st.unit = atomicAdd(a.work_counter, 1ull);
+    __syncthreads();
+    const uint64_t unit = st.unit;
+    if (unit >= a.nunits) return;
+
+    const uint32_t qi = a.unit_query[unit];
+    const PartDesc part = a.parts[a.unit_part[unit]];
+    const uint64_t row0 = part.row_off;
+    const uint32_t n = part.n;
+
+    // query slice in registers: lane holds dims [lane*4 + 128 v, +4)
+    float4 q[VPL];
+    {
+      const float* qp = a.queries + (uint64_t)qi * (uint64_t)a.dim;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int b = lane * 4 + 128 * v;
+        q[v].x = b + 0 < a.dim ? qp[b + 0] : 0.0f;
+        q[v].y = b + 1 < a.dim ? qp[b + 1] : 0.0f;
+        q[v].z = b + 2 < a.dim ? qp[b + 2] : 0.0f;
+        q[v].w = b + 3 < a.dim ? qp[b + 3] : 0.0f;
+      }
+    }
+
+    for (int i = tid; i < a.hsize; i += kThreads) table[i] = kEmpty;
+    __syncthreads();
+
+    int P = 0;
+    uint64_t thresh = ~0ull;
+    uint64_t visited = 0;
+
+    const int entries = a.entry_count < (int)n ? a.entry_count : (int)n;
+    int nf = 0;
+    // phase -1: entry nodes; phases 0..iters-1: frontier expansion
+    for (int it = -1; it < a.iters; ++it) {
+      int raw_total;
+      if (it < 0) {
+        raw_total = entries;
+      } else {
+        // ---- frontier: first `beam` unexpanded pool entries, in pool order
+        if (tid == 0) st.nf = 0;
+        __syncthreads();
+        for (int base = 0; base < P; base += kThreads) {
+          const int pos = base + tid;
+          const bool cand_f = pos < P && !(pool[pos] & 1ull);
+          const unsigned bal = __ballot_sync(full, cand_f);
+          if (lane == 0) st.warp_cnt[warp] = __popc(bal);
+          __syncthreads();
+          int before = st.nf;
+          int total = 0;
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) {
+            if (w < warp) before += st.warp_cnt[w];
+            total += st.warp_cnt[w];
+          }
+          const int rank = before + __popc(bal & lt_mask);
+          if (cand_f && rank < a.beam) {
+            const uint64_t key = pool[pos];
+            frontier[rank] = (uint32_t)(key >> 1) & 0x7FFFFFFFu;
+            pool[pos] = key | 1ull;
+          }
+          __syncthreads();
+          if (tid == 0) st.nf += total;
+          __syncthreads();
+          if (st.nf >= a.beam) break;
+        }
+        nf = st.nf < a.beam ? st.nf : a.beam;
+        if (nf == 0) break;  // graph_index.cpp:160
+        raw_total = nf * a.dg;
+      }
+
+      for (int cbase = 0; cbase < raw_total; cbase += kChunk) {
+        const int rcount = raw_total - cbase < kChunk ? raw_total - cbase : kChunk;
+        if (tid == 0) {
+          st.ncand = 0;
+          st.nsurv = 0;
+        }
+        // ---- gather raw ids (all loads first for MLP), then dedup
+        uint32_t ids[kRawPerThread];
+#pragma unroll
+        for (int j = 0; j < kRawPerThread; ++j) {
+          const int r = j * kThreads + tid;
+          ids[j] = kEmpty;
+          if (r < rcount) {
+            const int g = cbase + r;
+            if (it < 0) {
+              ids[j] = __ldg(a.entry + row0 + g);
+            } else {
+              const int f = g / a.dg, jj = g - f * a.dg;
+              ids[j] = __ldg(a.adjacency + (row0 + frontier[f]) * (uint64_t)a.dg + jj);
+            }
+          }
+        }
+        __syncthreads();  // st.ncand reset visible
+#pragma unroll
+        for (int j = 0; j < kRawPerThread; ++j) {
+          if (j * kThreads >= rcount) break;  // block-uniform
+          const bool isnew = ids[j] != kEmpty && visit_insert(table, hmask, ids[j]);
+          const unsigned bal = __ballot_sync(full, isnew);
+          int base = 0;
+          if (lane == 0 && bal) base = atomicAdd(&st.ncand, __popc(bal));
+          base = __shfl_sync(full, base, 0);
+          if (isnew) cand[base + __popc(bal & lt_mask)] = ids[j];
+        }
+        __syncthreads();
+        const int M = st.ncand;
+        visited += (uint64_t)M;
+
+        // ---- score new candidates: warp per vector, U in flight
+        for (int cb = warp * U; cb < M; cb += kWarps * U) {
+          float4 x[U][VPL];
+          uint32_t loc[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int ci = cb + u;
+            loc[u] = ci < M ? cand[ci] : 0u;
+            const float* row = a.vectors + (row0 + loc[u]) * (uint64_t)a.dpad;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              const int b = lane * 4 + 128 * v;
+              if (ci < M && b < a.dpad) x[u][v] = ldg_f4(row + b);
+              else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          ACC s[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            ACC acc = lane_partial<ACC, METRIC>(x[u][0], q[0]);
+#pragma unroll
+            for (int v = 1; v < VPL; ++v) acc += lane_partial<ACC, METRIC>(x[u][v], q[v]);
+            s[u] = warp_sum<ACC>(acc);
+          }
+          // lane u owns result u
+          uint64_t mykey = ~0ull;
+          bool pass = false;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (lane == u && cb + u < M) {
+              const float dist = METRIC == 0 ? (float)s[u] : (float)(-s[u]);
+              mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)loc[u] << 1);
+              pass = mykey < thresh;
+            }
+          }
+          const unsigned bal = __ballot_sync(full, pass);
+          int base = 0;
+          if (lane == 0 && bal) base = atomicAdd(&st.nsurv, __popc(bal));
+          base = __shfl_sync(full, base, 0);
+          if (pass) surv[base + __popc(bal & lt_mask)] = mykey;
+        }
+        __syncthreads();
+        const int S = st.nsurv;
+        __syncthreads();  // every thread has read the counters before the next reset
+        if (S == 0) continue;  // block-uniform
+
+        // ---- sort survivors, merge into the pool, truncate at cap
+        const int Sp = pow2_ceil(S);
+        for (int i = S + tid; i < Sp; i += kThreads) surv[i] = ~0ull;
+        __syncthreads();
+        bitonic_sort(surv, Sp);
+        for (int i = tid; i < P; i += kThreads) {
+          const uint64_t key = pool[i];
+          const int pos = i + lower_rank(surv, S, key);
+          if (pos < a.cap) pool_alt[pos] = key;
+        }
+        for (int j = tid; j < S; j += kThreads) {
+          const uint64_t key = surv[j];
+          const int pos = j + lower_rank(pool, P, key);
+          if (pos < a.cap) pool_alt[pos] = key;
+        }
+        __syncthreads();
+        {
+          uint64_t* t = pool;
+          pool = pool_alt;
+          pool_alt = t;
+        }
+        P = P + S < a.cap ? P + S : a.cap;
+        thresh = P == a.cap ? pool[a.cap - 1] : ~0ull;
+      }
+    }
+
+    // ---- final: global ids, re-sorted by (dist, gid), first min(k, P)
+    //      (graph_index.cpp:173-186).  Only entries whose dist ties the
+    //      want-th can reorder, so sort the prefix up to the last such tie.
+    const int want = a.k < P ? a.k : P;
+    if (want > 0) {
+      const uint32_t dk = (uint32_t)(pool[want - 1] >> 32);
+      int lo = want, hi = P;  // first index with dist > dk
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((uint32_t)(pool[mid] >> 32) <= dk) lo = mid + 1; else hi = mid;
+      }
+      const int m = lo;
+      const int mp = pow2_ceil(m);
+      for (int i = tid; i < mp; i += kThreads) {
+        if (i < m) {
+          const uint64_t key = pool[i];
+          const uint32_t local = (uint32_t)(key >> 1) & 0x7FFFFFFFu;
+          surv[i] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)__ldg(a.gids + row0 + local);
+        } else {
+          surv[i] = ~0ull;
+        }
+      }
+      __syncthreads();
+      bitonic_sort(surv, mp);
+      for (int i = tid; i < want; i += kThreads) {
+        const uint64_t key = surv[i];
+        a.out_ids[unit * (uint64_t)a.k + i] = (uint32_t)key;
+        a.out_dists[unit * (uint64_t)a.k + i] = ord2f((uint32_t)(key >> 32));
+      }
+    }
+    if (tid == 0) {
+      a.out_count[unit] = (uint32_t)want;
+      a.out_visited[unit] = visited;
+    }
+    __syncthreads();
+  }
+}
+
+template <int VPL, typename ACC, int METRIC>
+cudaError_t launch_t(const SearchArgs& a, int num_sms, int max_grid, cudaStream_t stream,
+                     int* grid_out) {
+  auto kern = search_kernel<VPL, ACC, METRIC>;
+  const size_t smem = search_smem_bytes(a.cap, a.chp, a.beam, a.hsize, a.hash_global == nullptr);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  uint64_t grid = (uint64_t)per_sm * (uint64_t)num_sms;
+  if (grid > a.nunits) grid = a.nunits;
+  if (max_grid > 0 && grid > (uint64_t)max_grid) grid = (uint64_t)max_grid;
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = (int)grid;
+  kern<<<(unsigned)grid, kThreads, smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <int VPL>
+cudaError_t launch_v(const SearchArgs& a, int metric, int accum, int num_sms, int mg,
+                     cudaStream_t s, int* g) {
+  if (accum == 0) {
+    return metric == 0 ? launch_t<VPL, double, 0>(a, num_sms, mg, s, g)
+                       : launch_t<VPL, double, 1>(a, num_sms, mg, s, g);
+  }
+  return metric == 0 ? launch_t<VPL, float, 0>(a, num_sms, mg, s, g)
+                     : launch_t<VPL, float, 1>(a, num_sms, mg, s, g);
+}
+
+}  // namespace
+
+size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_smem) {
+  size_t b = sizeof(uint64_t) * (2 * (size_t)cap + (size_t)chp);
+  b += sizeof(uint32_t) * ((size_t)kChunk + (size_t)((beam + 3) & ~3));
+  if (hash_in_smem) b += sizeof(uint32_t) * (size_t)hsize;
+  return b;
+}
+
+cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sms,
+                          int max_grid, cudaStream_t stream, int* grid_out) {
+  const int vpl = (a.dpad + 127) / 128;
+  switch (vpl) {
+    case 1: return launch_v<1>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 2: return launch_v<2>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 3:
+    case 4: return launch_v<4>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 5:
+    case 6: return launch_v<6>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 7:
+    case 8: return launch_v<8>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace dvsg

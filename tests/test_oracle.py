@@ -1,0 +1,137 @@
+"""CPU: pin the C restatement (oracle/dvs_oracle.c) against the reference.
+
+Two pins: the committed golden fixtures (made by tests/golden/make_golden.py
+from the reference's own compiled sources), and -- when oracle/_ref exists in
+this container -- the reference library itself on fresh seeded inputs.  The
+known-answer tests are the reference's own (test_graph_index.cpp,
+test_vector_core.cpp, test_kmeans.cpp), restated on the oracle.
+"""
+import numpy as np
+import pytest
+
+
+def _pick(res, i):
+    return [res[f"ids{i}"], res[f"dists{i}"], res[f"counts{i}"], res[f"visited{i}"]]
+
+
+def test_mt19937_64_known_value(oracle):
+    # std::mt19937_64 default-seed 10000th output is 9981545732273789042 (C++ std)
+    import ctypes
+    from oracle.oracle import HERE  # noqa: F401
+    g = (ctypes.c_uint64 * 313)()
+    oracle.lib.dvso_mt64_seed.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+    oracle.lib.dvso_mt64_next.restype = ctypes.c_uint64
+    oracle.lib.dvso_mt64_next.argtypes = [ctypes.c_void_p]
+    oracle.lib.dvso_mt64_seed(g, 5489)
+    x = 0
+    for _ in range(10000):
+        x = oracle.lib.dvso_mt64_next(g)
+    assert x == 9981545732273789042
+
+
+def test_squared_l2_kats(oracle):
+    # test_vector_core.cpp:69-76
+    assert oracle.squared_l2([0, 0], [3, 4]) == 25.0
+    assert oracle.squared_l2([3, 4], [3, 4]) == 0.0
+    assert oracle.squared_l2([1, 2, 3], [4, 6, 3]) == 25.0
+
+
+@pytest.mark.parametrize("fixture", ["g1_uniform.npz", "g2_siftlike.npz"])
+def test_oracle_matches_golden_search(oracle, golden, fixture):
+    g = golden(fixture)
+    v, adj, eo, q = g["vectors"], g["adjacency"], g["entry_order"], g["queries"]
+    gids = g["gids"] if "gids" in g.files else np.arange(v.shape[0], dtype=np.uint32)
+    assert (oracle.compute_entry_order(v) == eo).all()
+    assert (oracle.build_graph(v, adj.shape[1]) == adj).all()
+    for i, (I, w, k, E) in enumerate(g["params"]):
+        got = oracle.beam_search(v, gids, adj, eo, q, int(I), int(w), int(k), int(E))
+        want = _pick(g, i)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b), (fixture, i)
+
+
+def test_oracle_matches_golden_brute_force(oracle, golden):
+    g = golden("g2_siftlike.npz")
+    ids, d = oracle.brute_force_topk(g["vectors"], g["queries"], 10)
+    assert np.array_equal(ids, g["truth_ids"]) and np.array_equal(d, g["truth_dists"])
+
+
+def _fnsy_index(path):
+    from fnsy import read_fnsy
+    return read_fnsy(path)
+
+
+def test_oracle_matches_golden_pipeline(oracle, golden):
+    from fnsy import G3_FNSY
+    idx = _fnsy_index(G3_FNSY)
+    res = golden("g3_mixture.npz")
+    q = res["queries"]
+    eo = np.concatenate([oracle.compute_entry_order(gr.vectors) for gr in idx.graphs])
+    assert np.array_equal(eo, res["entry_orders"])
+    assert np.array_equal(oracle.assign_top_c(idx.centroids, q, 3), res["assign3"])
+    for fo in (1, 2, 3):
+        ids, d, c, vecs, vt = oracle.run_pipeline(idx, q, 6, 16, 10, 16, fo, 4, batch_index=1)
+        assert np.array_equal(ids, res[f"ids_f{fo}"])
+        assert np.array_equal(d, res[f"dists_f{fo}"])
+        assert np.array_equal(c, res[f"counts_f{fo}"])
+        assert np.array_equal(vecs, res[f"vectors_f{fo}"])
+        assert vt == int(res[f"visited_f{fo}"])
+
+
+def test_oracle_matches_golden_combine(oracle, golden):
+    g = golden("g4_combine.npz")
+    for i in range(int(g["ncases"])):
+        oi, od = oracle.combine_results(g[f"c{i}_ids"], g[f"c{i}_dists"], g[f"c{i}_counts"],
+                                        int(g[f"c{i}_k"]))
+        assert np.array_equal(oi, g[f"c{i}_oi"]) and np.array_equal(od, g[f"c{i}_od"])
+
+
+def test_oracle_vs_reference_fresh_inputs(oracle, ref):
+    v = oracle.random_dataset(1500, 12, 901)
+    g, adj, eo = ref.build_graph(v, 24)
+    assert np.array_equal(oracle.build_graph(v, 24), adj)
+    q = oracle.random_dataset(150, 12, 902)
+    gids = np.arange(1500, dtype=np.uint32)
+    for (I, w, k, E) in [(6, 32, 10, 32), (3, 5, 7, 2), (1, 1, 1, 1), (10, 8, 40, 1500)]:
+        a = oracle.beam_search(v, gids, adj, eo, q, I, w, k, E)
+        b = g.beam_search(q, I, w, k, E)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+def test_oracle_vs_reference_assign_and_topk(oracle, ref):
+    q = oracle.random_dataset(25, 8, 45, -1000, 1000)
+    c = oracle.random_dataset(16, 8, 46, -1000, 1000)
+    assert np.array_equal(oracle.assign_top_c(c, q, 16), ref.assign_top_c(c, q, 16))
+    db = oracle.random_dataset(100, 8, 21)
+    qs = oracle.random_dataset(20, 8, 22)
+    a = oracle.brute_force_topk(db, qs, 10)
+    b = ref.brute_force_topk(db, qs, 10)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ---- reference KATs restated on the oracle (test_graph_index.cpp) -----------
+
+def test_kat_collinear_and_cyclic(oracle):
+    adj = oracle.build_graph(np.array([[0], [1], [10]], np.float32), 1)  # :32-38
+    assert adj[:, 0].tolist() == [1, 0, 1]
+    adj = oracle.build_graph(np.array([[0, 0], [1, 1]], np.float32), 4)  # :40-47
+    assert adj[0].tolist() == [1] * 4 and adj[1].tolist() == [0] * 4
+
+
+def test_kat_complete_graph_equals_brute_force(oracle):
+    v = oracle.random_dataset(9, 5, 53)  # :100-120
+    adj = oracle.build_graph(v, 12)
+    eo = oracle.compute_entry_order(v)
+    q = oracle.random_dataset(10, 5, 54)
+    ids, d, c, _ = oracle.beam_search(v, np.arange(9, dtype=np.uint32), adj, eo, q, 1, 1, 5, 1)
+    bi, bd = oracle.brute_force_topk(v, q, 5)
+    assert np.array_equal(ids, bi) and np.array_equal(d, bd)
+
+
+def test_kat_single_vector_partition(oracle):
+    v = np.array([[1, 2, 3]], np.float32)  # :76-90
+    adj = oracle.build_graph(v, 3)
+    ids, d, c, vis = oracle.beam_search(v, np.array([42], np.uint32), adj, np.array([0], np.uint32),
+                                        np.zeros((1, 3), np.float32), 2, 2, 5, 1)
+    assert c[0] == 1 and ids[0, 0] == 42 and vis[0] == 1
