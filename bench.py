@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""bench.py -- QPS of the batched graph search at recall@10 >= 0.95 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dvsg|reference]
+
+One step = one run_pipeline pass (simulator.cpp:245-337 functional part:
+assign -> route -> K1 beam search -> combine -> attach hit vectors) over one
+batch of 100k synthetic SIFT-like queries against the 1M x 128 kNN-32 graph
+(BASELINE.json configs[1] at N=1: the graph in one partition; I=6, w=64,
+entry=64, k=10 calibrated to recall@10 >= 0.95 on this data).
+
+`value`  : device-resident queries, CUDA events on the library's stream, L2
+           flushed (256 MiB write) before every step, max over ranks.
+`e2e`    : the same step through the public host-buffer call
+           (dvsg_run_pipeline: pinned host queries in, ids/dists/counts/hit
+           vectors out; H2D and D2H inside the timed region).
+`roofline`: K1 algorithmic bytes (visited*4d + expanded*4*d_g + 4d per unit,
+           SURVEY 8d) / K1 event time, against MEASURED_PEAKS.json hbm_gbs.
+`cpu_baseline`: the reference's own run_pipeline (oracle/_ref, compiled from
+           /root/reference sources) on a bounded query sample, all host cores.
+
+N > 1 (torchrun, one rank per GPU): each rank holds a full replica of the
+index and searches its own 100k-query batch ("replicas": weak scaling); the
+sharded frontier-exchange mode is not in this round.
+`--impl reference`: rank 0 times the reference CPU path (same config and
+metric), other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["dvsg", "reference"], default="dvsg")
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--nq", type=int, default=100_000)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--rank-latent", type=int, default=16)
+    ap.add_argument("--degree", type=int, default=32)
+    ap.add_argument("--iterations", type=int, default=6)
+    ap.add_argument("--beam", type=int, default=64)
+    ap.add_argument("--k", type=int, default=10)
+    ap.add_argument("--entry", type=int, default=64)
+    ap.add_argument("--accum", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--recall-sample", type=int, default=2000)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cache", default="/tmp/dvsg_bench_cache")
+    return ap.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (getattr(self, "out", "") or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def workload(args, rank: int, ctx):
+    """Data + queries + index (graph cached by config under args.cache)."""
+    from paper_2512_02278_b200 import synth
+    from paper_2512_02278_b200.api import BuiltIndex, GraphIndex, compute_entry_order
+    t0 = time.time()
+    data = synth.sift_like(args.n, args.dim, args.rank_latent, seed=1)
+    queries = synth.sift_like_queries(args.nq, args.dim, args.rank_latent, data_seed=1, seed=2 + rank)
+    os.makedirs(args.cache, exist_ok=True)
+    tag = f"n{args.n}_d{args.dim}_r{args.rank_latent}_g{args.degree}"
+    adj_path = os.path.join(args.cache, f"adj_{tag}.npy")
+    eo_path = os.path.join(args.cache, f"eo_{tag}.npy")
+    if os.path.isfile(adj_path) and os.path.isfile(eo_path):
+        adj, eo = np.load(adj_path), np.load(eo_path)
+    else:
+        adj = ctx.build_graph(data, args.degree)       # K6, exact on integer data
+        eo = compute_entry_order(data)                 # graph_index.cpp:21-44
+        tmp = adj_path + f".{os.getpid()}.npy"
+        np.save(tmp, adj)
+        os.replace(tmp, adj_path)
+        tmp = eo_path + f".{os.getpid()}.npy"
+        np.save(tmp, eo)
+        os.replace(tmp, eo_path)
+    gids = np.arange(args.n, dtype=np.uint32)
+    cents = data.mean(0, dtype=np.float64).astype(np.float32)[None, :]
+    index = BuiltIndex(cents, np.zeros(1, np.uint32), 1, args.degree,
+                       [GraphIndex(data, gids, args.degree, adj, eo)])
+    log(f"[bench] workload ready in {time.time() - t0:.1f}s")
+    return data, queries, index
+
+
+def recall(data, queries, ids, counts, k):
+    from paper_2512_02278_b200 import synth
+    truth = synth.brute_force_gt(data, queries, k)
+    return synth.recall_at_k(ids, counts, truth, k)
+
+
+# ---------------------------------------------------------------------------
+def reference_arm(args, data, queries, index, nthreads, seconds, min_q=64):
+    """Time the reference's own run_pipeline on a bounded sample."""
+    from oracle.oracle import Oracle, Ref, have_ref
+    kind = "reference" if have_ref() else "port"
+    g = index.graphs[0]
+    if kind == "reference":
+        ref = Ref()
+        ridx = ref.index_from_arrays(index.centroids, index.cluster_to_rank, 1, args.degree,
+                                     [(g.vectors, g.adjacency, g.global_ids)])
+
+        def run(qs):
+            return ridx.run_pipeline(qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
+                                     nthreads=nthreads, with_vectors=True)
+    else:
+        o = Oracle()
+
+        def run(qs):
+            return o.run_pipeline(index, qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
+                                  nthreads=nthreads, with_vectors=True)
+    # size the sample so one pass is ~`seconds` of CPU wall time
+    probe = queries[:max(min_q, 2 * nthreads)]
+    t0 = time.perf_counter()
+    run(probe)
+    dt = time.perf_counter() - t0
+    per_q = dt / probe.shape[0]
+    n = int(min(queries.shape[0], max(probe.shape[0], seconds / max(per_q, 1e-9))))
+    return kind, run, n
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference_impl(args, world, rank):
+    """--impl reference: rank 0 times the reference CPU implementation."""
+    if rank != 0:
+        return
+    import paper_2512_02278_b200 as dvs
+    ctx = dvs.Context(0)  # setup only: builds the shared graph if not cached
+    data, queries, index = workload(args, 0, ctx)
+    ctx.close()
+    nthreads = os.cpu_count() or 1
+    kind, run, n = reference_arm(args, data, queries, index, nthreads, args.cpu_seconds)
+    sample = queries[:n]
+    run(sample[: min(n, 4 * nthreads)])  # warm caches / page in the index
+    times = []
+    res = None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        res = run(sample)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    qps = n * args.steps / total
+    rec = recall(data, sample[: min(n, args.recall_sample)], res[0], res[2], args.k)
+    line = {
+        "impl": "reference", "metric": "QPS at recall@10>=0.95", "value": qps, "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, world, rec),
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": nthreads, "kind": kind,
+                         "sample": f"{n} of the {args.nq} queries per step, run_pipeline C=1 "
+                                   f"(simulator.cpp:245-366) in {nthreads} threads",
+                         "cpu_model": cpu_model()},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world, rec):
+    return {
+        "workload": "BASELINE configs[1] at N=1: SIFT-like synthetic 1M x 128 (integer-valued f32, "
+                    "rank-16 latent), exact kNN-32 graph in 1 partition, 100k-query batch per GPU, "
+                    "top-10, beam 64, I=6, entry 64",
+        "n": args.n, "dim": args.dim, "degree": args.degree, "queries_per_step_per_gpu": args.nq,
+        "iterations": args.iterations, "beam_width": args.beam, "k": args.k,
+        "entry_count": args.entry, "partitions": 1, "accum": args.accum,
+        "recall_at_10": None if rec is None else round(rec, 4),
+        "l2": "256 MiB buffer written before every timed step",
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+    }
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_impl(args, world, rank)
+
+    import torch
+    import paper_2512_02278_b200 as dvs
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    ctx = dvs.Context(local)
+    data, queries, index = workload(args, rank, ctx)
+    ctx.load_index(index)
+    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+    nq, dim, k = args.nq, args.dim, args.k
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    d_q = torch.from_numpy(queries).to(dev)
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    d_counts = torch.empty((nq,), dtype=torch.int32, device=dev)
+    d_vecs = torch.empty((nq, k, dim), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.run_pipeline_device(d_q.data_ptr(), nq, dim, p, 1, d_ids.data_ptr(), d_dists.data_ptr(),
+                                d_counts.data_ptr(), d_vecs.data_ptr())
+
+    ctx.set_timing(True)
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+
+    # ---- timed region: K steps, L2 flushed before each -------------------------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k1_ms, vis_tot, exp_tot, units_tot = 0.0, 0, 0, 0
+    launches0 = ctx.kernel_launches()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+            st = ctx.last_search_stats()      # syncs the stream
+            k1_ms += ctx.last_timings()["search_ms"]
+            vis_tot += st["visited"]
+            exp_tot += st["expanded"]
+            units_tot += st["units"]
+        torch.cuda.synchronize()
+    launches = ctx.kernel_launches() - launches0
+    step_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t_local = torch.tensor([step_ms, k1_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.barrier()
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    total_ms, k1_max_ms = float(t_local[0]), float(t_local[1])
+
+    # ---- parity sample + recall (outside timing) ------------------------------------
+    ids_h = d_ids.cpu().numpy().view(np.uint32)
+    cnt_h = d_counts.cpu().numpy().view(np.uint32)
+    rec = None
+    if rank == 0:
+        s = min(args.recall_sample, nq)
+        rec = recall(data, queries[:s], ids_h[:s], cnt_h[:s], k)
+
+    # ---- e2e through the public host-buffer call ------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        keep = []
+
+        def pin(shape, dt):
+            t = torch.empty(shape, dtype=dt, pin_memory=True)
+            keep.append(t)
+            return t.numpy()
+
+        hq = pin((nq, dim), torch.float32)
+        hq[:] = queries
+        out = {"ids": pin((nq, k), torch.int32).view(np.uint32), "dists": pin((nq, k), torch.float32),
+               "counts": pin((nq,), torch.int32).view(np.uint32), "vectors": pin((nq, k, dim), torch.float32)}
+        ctx.run_pipeline(hq, p, 1, 1, 0, True, out)  # warm
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            ev0[i].record(stream)
+            ctx.run_pipeline(hq, p, 1, 1, 0, True, out)
+            ev1[i].record(stream)
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        assert np.array_equal(out["ids"], ids_h) and np.array_equal(out["counts"], cnt_h), \
+            "host-buffer and device-pointer paths disagree"
+        h2d = hq.nbytes
+        d2h = out["ids"].nbytes + out["dists"].nbytes + out["counts"].nbytes + out["vectors"].nbytes + 4 + 8
+        e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(e_ms[0]) / args.steps}
+
+    # ---- CPU baseline (rank 0, N=1) ---------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            nthreads = os.cpu_count() or 1
+            kind, run, n = reference_arm(args, data, queries, index, nthreads, args.cpu_seconds)
+            t0 = time.perf_counter()
+            r = run(queries[:n])
+            dt = time.perf_counter() - t0
+            same = np.array_equal(r[0], ids_h[:n]) and np.array_equal(r[2], cnt_h[:n])
+            cpu = {"value": n / dt, "unit": "queries/s", "cores": nthreads, "kind": kind,
+                   "sample": f"first {n} of the {nq} step queries, run_pipeline C=1, {nthreads} threads",
+                   "cpu_model": cpu_model(), "ids_identical_to_gpu": bool(same)}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "unavailable",
+                   "sample": f"failed: {ex}"}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = peaks()
+    d4 = 4 * dim
+    alg_bytes = vis_tot * d4 + exp_tot * 4 * args.degree + units_tot * d4
+    achieved = alg_bytes / args.steps / (k1_max_ms / args.steps / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.isfile(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config_key") == f"n{args.n}_q{nq}_w{args.beam}_I{args.iterations}_{args.accum}":
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    value = nq * world * args.steps / (total_ms / 1e3)
+    line = {
+        "metric": "QPS at recall@10>=0.95", "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(args, world, rec),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "dvsg::search_kernel (K1)",
+                     "k1_ms_per_step": k1_max_ms / args.steps,
+                     "alg_bytes_per_step": alg_bytes / args.steps,
+                     "visited_per_query": vis_tot / max(units_tot, 1),
+                     "expanded_per_query": exp_tot / max(units_tot, 1)},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

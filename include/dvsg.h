@@ -173,6 +173,11 @@ dvsg_status dvsg_last_timings(dvsg_ctx *ctx, float *search_ms, float *assign_ms,
                               float *combine_ms, float *total_ms);
 /* Number of library kernels launched by this context since creation. */
 uint64_t dvsg_kernel_launches(dvsg_ctx *ctx);
+/* Totals of the last K1 launch: units searched, vectors scored (the
+ * reference's visited counter) and frontier nodes expanded -- the inputs of
+ * the algorithmic byte count visited*4d + expanded*4*d_g + 4d per unit. */
+dvsg_status dvsg_last_search_stats(dvsg_ctx *ctx, uint64_t *units, uint64_t *visited,
+                                   uint64_t *expanded);
 
 #ifdef __cplusplus
 }

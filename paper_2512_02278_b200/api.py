@@ -267,15 +267,30 @@ class Context:
         return oi, od, oc
 
     def run_pipeline(self, queries, p: SearchParams, fanout: int, ranks: int,
-                     batch_index: int = 0, with_vectors: bool = True) -> PipelineResult:
+                     batch_index: int = 0, with_vectors: bool = True,
+                     out: Optional[dict] = None) -> PipelineResult:
+        """Host buffers in and out (H2D/D2H inside).  `out` may hold
+        preallocated (e.g. pinned) arrays: ids, dists, counts, vectors."""
         q = _f32(queries, 2)
         nq, dim = q.shape
         cp = p.to_c()
         k = max(int(p.k), 1)
-        ids = np.zeros((nq, k), np.uint32)
-        dists = np.zeros((nq, k), np.float32)
-        counts = np.zeros(nq, np.uint32)
-        vecs = np.zeros((nq, k, dim), np.float32) if with_vectors else None
+        out = out or {}
+        ids = out.get("ids")
+        ids = np.zeros((nq, k), np.uint32) if ids is None else ids
+        dists = out.get("dists")
+        dists = np.zeros((nq, k), np.float32) if dists is None else dists
+        counts = out.get("counts")
+        counts = np.zeros(nq, np.uint32) if counts is None else counts
+        vecs = out.get("vectors")
+        if vecs is None and with_vectors:
+            vecs = np.zeros((nq, k, dim), np.float32)
+        if not with_vectors:
+            vecs = None
+        for a, shape, dt in ((ids, (nq, k), np.uint32), (dists, (nq, k), np.float32),
+                             (counts, (nq,), np.uint32)):
+            if a.shape != shape or a.dtype != dt or not a.flags.c_contiguous:
+                raise InvalidArgument("run_pipeline: bad output buffer")
         vt = ctypes.c_uint64(0)
         check(lib.dvsg_run_pipeline(self._h, _ptr(q), nq, dim, ctypes.byref(cp), int(fanout),
                                     int(ranks), int(batch_index), _ptr(ids), _ptr(dists),
@@ -287,6 +302,22 @@ class Context:
         adj = np.zeros((v.shape[0], int(out_degree)), np.uint32)
         check(lib.dvsg_build_graph(self._h, _ptr(v), v.shape[0], v.shape[1], int(out_degree), _ptr(adj)))
         return adj
+
+    def last_search_stats(self):
+        u, v, e = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.dvsg_last_search_stats(self._h, ctypes.byref(u), ctypes.byref(v), ctypes.byref(e)))
+        return {"units": u.value, "visited": v.value, "expanded": e.value}
+
+    def run_pipeline_device(self, d_queries: int, nq: int, dim: int, p: SearchParams, fanout: int,
+                            d_ids: int, d_dists: int, d_counts: int, d_vectors: int = 0,
+                            d_visited: int = 0) -> None:
+        """Asynchronous on self.stream; all arguments are device addresses."""
+        cp = p.to_c()
+        check(lib.dvsg_run_pipeline_device(self._h, ctypes.c_void_p(d_queries), int(nq), int(dim),
+                                           ctypes.byref(cp), int(fanout), ctypes.c_void_p(d_ids),
+                                           ctypes.c_void_p(d_dists), ctypes.c_void_p(d_counts),
+                                           ctypes.c_void_p(d_vectors or None),
+                                           ctypes.c_void_p(d_visited or None)))
 
     # ---- timing --------------------------------------------------------------
     def set_timing(self, on: bool) -> None:

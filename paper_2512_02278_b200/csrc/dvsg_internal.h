@@ -41,6 +41,7 @@ struct SearchArgs {
   uint32_t* out_count;    // nunits
   uint64_t* out_visited;  // nunits
   unsigned long long* work_counter;
+  unsigned long long* stats;  // [0] units, [1] visited, [2] expanded (frontier nodes); nullable
 };
 
 // Launch K1 (search_kernel.cu).  Returns a cudaError_t.
@@ -52,9 +53,10 @@ size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_sme
 constexpr int kChunk = 2048;  // raw candidates per dedup/score/merge chunk (8 per thread)
 
 // K5 assign (route_kernels.cu): nq x c cluster ids, exact fp64 expanded form.
+// scratch: nq x clusters u64 keys.
 cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const float* cents,
                           const double* cent_norms, int clusters, int c, uint32_t* out,
-                          cudaStream_t stream);
+                          uint64_t* scratch, cudaStream_t stream);
 // K4 combine: per query merge nparts sorted partial lists (stride entries each).
 cudaError_t launch_combine(uint64_t nq, int nparts, const uint32_t* ids, const float* dists,
                            const uint32_t* counts, int stride, int k, uint32_t* out_ids,

@@ -134,15 +134,19 @@ struct dvsg_ctx {
   DevBuf<float> u_dists;
   DevBuf<uint64_t> u_visited;
   DevBuf<uint32_t> hash;
-  DevBuf<unsigned long long> counter;
+  DevBuf<unsigned long long> counter;  // [0] work counter, [1..3] stats
+  DevBuf<uint64_t> assign_scratch;
+  unsigned long long last_stats[3] = {0, 0, 0};
+  bool stats_pending = false;
   DevBuf<int> err_flag;
-  DevBuf<float> io_f;
+  DevBuf<float> io_f, io_dists, io_vecs;
   DevBuf<uint32_t> io_u;
   DevBuf<uint64_t> io_u64;
   // timing
   bool timing = false;
   cudaEvent_t ev[8] = {};
   float t_search = 0, t_assign = 0, t_combine = 0, t_total = 0;
+  int timing_pending = 0;  // 1: search only, 2: pipeline
   std::atomic<uint64_t> launches{0};
 };
 
@@ -284,9 +288,11 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   a.out_dists = d_dists;
   a.out_count = d_count;
   a.out_visited = d_visited;
-  c->counter.reserve(1, c->stream);
+  c->counter.reserve(4, c->stream);
   a.work_counter = c->counter.p;
-  cuda_check(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned long long), c->stream), "counter reset");
+  a.stats = c->counter.p + 1;
+  cuda_check(cudaMemsetAsync(c->counter.p, 0, 4 * sizeof(unsigned long long), c->stream), "counter reset");
+  c->stats_pending = true;
   int max_grid = 0;
   if (!in_smem) {
     // one L2-resident region per persistent CTA
@@ -297,7 +303,10 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   if (c->timing) cudaEventRecord(c->ev[0], c->stream);
   int grid = 0;
   cuda_check(dvsg::launch_search(a, p->metric, p->accum, c->num_sms, max_grid, c->stream, &grid), "search kernel launch");
-  if (c->timing) cudaEventRecord(c->ev[1], c->stream);
+  if (c->timing) {
+    cudaEventRecord(c->ev[1], c->stream);
+    c->timing_pending = 1;
+  }
   c->launches += 1;
 }
 
@@ -353,7 +362,8 @@ void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const 
   c->err_flag.reserve(1, c->stream);
   cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
-  cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->stream), "assign");
+  c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
+  cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->assign_scratch.p, c->stream), "assign");
   cuda_check(dvsg::launch_route(c->assign.p, nq, fanout, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
   c->launches += 2;
@@ -366,7 +376,10 @@ void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const 
     cuda_check(dvsg::launch_gather_vectors(d_ids, d_count, nq, p->k, c->d_locator.p, c->vec.p, c->dim, c->dpad, d_vecs, c->stream), "gather vectors");
     c->launches += 1;
   }
-  if (c->timing) cudaEventRecord(c->ev[5], c->stream);
+  if (c->timing) {
+    cudaEventRecord(c->ev[5], c->stream);
+    c->timing_pending = 2;
+  }
 }
 
 void check_err_flag(dvsg_ctx* c, const char* what) {
@@ -378,6 +391,7 @@ void check_err_flag(dvsg_ctx* c, const char* what) {
 
 void read_timings(dvsg_ctx* c, bool pipeline) {
   if (!c->timing) return;
+  c->timing_pending = 0;
   cudaEventSynchronize(c->ev[pipeline ? 5 : 1]);
   cudaEventElapsedTime(&c->t_search, c->ev[0], c->ev[1]);
   if (pipeline) {
@@ -692,7 +706,8 @@ dvsg_status dvsg_assign_top_c(dvsg_ctx* c, const float* queries, uint64_t nq, in
     if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
     const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
     c->assign.reserve(nq * (uint64_t)cc, c->stream);
-    cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, c->assign.p, c->stream), "assign");
+    c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
+    cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, c->assign.p, c->assign_scratch.p, c->stream), "assign");
     c->launches += 1;
     cuda_check(cudaMemcpyAsync(out, c->assign.p, nq * (uint64_t)cc * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaStreamSynchronize(c->stream), "assign");
@@ -753,7 +768,8 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
     const uint64_t k = (uint64_t)p->k;
     const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
     c->io_u.reserve(nq * k + nq, c->stream);
-    DevBuf<float> od, ov;
+    DevBuf<float>& od = c->io_dists;
+    DevBuf<float>& ov = c->io_vecs;
     od.reserve(nq * k, c->stream);
     if (out_vectors) ov.reserve(nq * k * (uint64_t)dim, c->stream);
     c->u_visited.reserve(nq * (uint64_t)fanout, c->stream);
@@ -762,12 +778,15 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
     c->io_u64.reserve(1, c->stream);
     cuda_check(dvsg::launch_reduce_u64(c->u_visited.p, nq * (uint64_t)fanout, reinterpret_cast<unsigned long long*>(c->io_u64.p), c->stream), "reduce");
     c->launches += 1;
-    check_err_flag(c, "route: cluster id outside placement / not resident, or combine_results: partial list not sorted");
-    cuda_check(cudaMemcpy(out_ids, c->io_u.p, nq * k * 4, cudaMemcpyDeviceToHost), "D2H");
-    cuda_check(cudaMemcpy(out_dists, od.p, nq * k * 4, cudaMemcpyDeviceToHost), "D2H");
-    cuda_check(cudaMemcpy(out_count, c->io_u.p + nq * k, nq * 4, cudaMemcpyDeviceToHost), "D2H");
-    if (out_vectors) cuda_check(cudaMemcpy(out_vectors, ov.p, nq * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost), "D2H");
-    if (visited_total) cuda_check(cudaMemcpy(visited_total, c->io_u64.p, 8, cudaMemcpyDeviceToHost), "D2H");
+    int flag = 0;
+    cuda_check(cudaMemcpyAsync(&flag, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_ids, c->io_u.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_dists, od.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_count, c->io_u.p + nq * k, nq * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (out_vectors) cuda_check(cudaMemcpyAsync(out_vectors, ov.p, nq * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    if (visited_total) cuda_check(cudaMemcpyAsync(visited_total, c->io_u64.p, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "run_pipeline");
+    if (flag) fail(DVSG_EINTERNAL, "route: cluster id outside placement / not resident, or combine_results: partial list not sorted");
     read_timings(c, true);
   });
 }
@@ -812,6 +831,7 @@ dvsg_status dvsg_set_timing(dvsg_ctx* c, int enabled) {
 
 dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, float* combine_ms, float* total_ms) {
   return guarded([&] {
+    if (c->timing_pending) read_timings(c, c->timing_pending == 2);
     if (search_ms) *search_ms = c->t_search;
     if (assign_ms) *assign_ms = c->t_assign;
     if (combine_ms) *combine_ms = c->t_combine;
@@ -820,6 +840,20 @@ dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, f
 }
 
 uint64_t dvsg_kernel_launches(dvsg_ctx* c) { return c ? c->launches.load() : 0; }
+
+dvsg_status dvsg_last_search_stats(dvsg_ctx* c, uint64_t* units, uint64_t* visited, uint64_t* expanded) {
+  return guarded([&] {
+    set_device(c);
+    if (c->stats_pending) {
+      cuda_check(cudaMemcpyAsync(c->last_stats, c->counter.p + 1, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream), "stats");
+      cuda_check(cudaStreamSynchronize(c->stream), "stats");
+      c->stats_pending = false;
+    }
+    if (units) *units = c->last_stats[0];
+    if (visited) *visited = c->last_stats[1];
+    if (expanded) *expanded = c->last_stats[2];
+  });
+}
 
 // ---- FNSY v1 -------------------------------------------------------------
 dvsg_status dvsg_load_index_file(dvsg_ctx* c, const char* path, int rank) {

@@ -171,17 +171,12 @@ __global__ void reduce_u64_kernel(const uint64_t* __restrict__ in, uint64_t n,
 
 cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const float* cents,
                           const double* cent_norms, int clusters, int c, uint32_t* out,
-                          cudaStream_t stream) {
+                          uint64_t* scratch, cudaStream_t stream) {
   if (nq == 0) return cudaSuccess;
-  uint64_t* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, sizeof(uint64_t) * nq * (uint64_t)clusters, stream);
-  if (e != cudaSuccess) return e;
   const int wpb = 4;
   assign_kernel<<<(unsigned)((nq + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
       queries, nq, dim, cents, cent_norms, clusters, c, scratch, out);
-  e = cudaGetLastError();
-  cudaFreeAsync(scratch, stream);
-  return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,

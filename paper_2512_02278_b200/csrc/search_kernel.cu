@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
     int P = 0;
     uint64_t thresh = ~0ull;
     uint64_t visited = 0;
+    uint64_t expanded = 0;
 
     const int entries = a.entry_count < (int)n ? a.entry_count : (int)n;
     int nf = 0;
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
         }
         nf = st.nf < a.beam ? st.nf : a.beam;
         if (nf == 0) break;  // graph_index.cpp:160
+        expanded += (uint64_t)nf;
         raw_total = nf * a.dg;
       }
 
@@ -392,6 +394,11 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
     if (tid == 0) {
       a.out_count[unit] = (uint32_t)want;
       a.out_visited[unit] = visited;
+      if (a.stats) {
+        atomicAdd(a.stats + 0, 1ull);
+        atomicAdd(a.stats + 1, (unsigned long long)visited);
+        atomicAdd(a.stats + 2, (unsigned long long)expanded);
+      }
     }
     __syncthreads();
   }
