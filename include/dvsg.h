@@ -178,6 +178,9 @@ uint64_t dvsg_kernel_launches(dvsg_ctx *ctx);
  * the algorithmic byte count visited*4d + expanded*4*d_g + 4d per unit. */
 dvsg_status dvsg_last_search_stats(dvsg_ctx *ctx, uint64_t *units, uint64_t *visited,
                                    uint64_t *expanded);
+/* Raw K1 counters of the last launch (16 u64; [0] work counter, [1..3] the
+ * stats above, [3..] kernel-variant debug counters, zero in release builds). */
+dvsg_status dvsg_debug_counters(dvsg_ctx *ctx, uint64_t *out16);
 
 #ifdef __cplusplus
 }

@@ -288,10 +288,10 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   a.out_dists = d_dists;
   a.out_count = d_count;
   a.out_visited = d_visited;
-  c->counter.reserve(4, c->stream);
+  c->counter.reserve(16, c->stream);
   a.work_counter = c->counter.p;
   a.stats = c->counter.p + 1;
-  cuda_check(cudaMemsetAsync(c->counter.p, 0, 4 * sizeof(unsigned long long), c->stream), "counter reset");
+  cuda_check(cudaMemsetAsync(c->counter.p, 0, 16 * sizeof(unsigned long long), c->stream), "counter reset");
   c->stats_pending = true;
   int max_grid = 0;
   if (!in_smem) {
@@ -840,6 +840,15 @@ dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, f
 }
 
 uint64_t dvsg_kernel_launches(dvsg_ctx* c) { return c ? c->launches.load() : 0; }
+
+dvsg_status dvsg_debug_counters(dvsg_ctx* c, uint64_t* out16) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->counter.p) fail(DVSG_EINVAL, "no search launched yet");
+    cuda_check(cudaMemcpyAsync(out16, c->counter.p, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream), "counters");
+    cuda_check(cudaStreamSynchronize(c->stream), "counters");
+  });
+}
 
 dvsg_status dvsg_last_search_stats(dvsg_ctx* c, uint64_t* units, uint64_t* visited, uint64_t* expanded) {
   return guarded([&] {

@@ -63,47 +63,155 @@ __device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uin
   }
 }
 
-// number of elements of sorted arr[0..len) strictly below key
-__device__ __forceinline__ int lower_rank(const uint64_t* arr, int len, uint64_t key) {
-  int lo = 0, hi = len;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (arr[mid] < key) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
-// Block-wide ascending bitonic sort of s[0..n), n a power of two.
-__device__ void bitonic_sort(uint64_t* s, int n) {
-  const int tid = threadIdx.x;
-  for (int kk = 2; kk <= n; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < n; i += kThreads) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t x = s[i], y = s[ixj];
-          const bool up = (i & kk) == 0;
-          if ((x > y) == up) {
-            s[i] = y;
-            s[ixj] = x;
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a < b ? b : a; }
+
+// Register-tiled bitonic sort of N = KPT * NT keys, ascending.  Element
+// e = t * KPT + r lives in x[r] of thread t.  Partners closer than KPT are in
+// the same thread (register compare-swap), closer than 32 * KPT in the same
+// warp (shuffles), the rest in other warps: only those log2(NT/32) * (...)
+// stages go through shared memory (r-major, conflict-free) with a barrier.
+template <int KPT, int NT>
+__device__ __forceinline__ void bitonic_regs(uint64_t (&x)[KPT], int t, uint64_t* s) {
+  constexpr int LOGN = ilog2(KPT * NT);
+#pragma unroll
+  for (int lk = 1; lk <= LOGN; ++lk) {
+    const int k = 1 << lk;
+#pragma unroll
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const int j = 1 << lj;
+      if (j < KPT) {
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+          const int r2 = r ^ j;
+          if (r2 > r) {
+            const bool up = ((t * KPT + r) & k) == 0;
+            const uint64_t lo = umin64(x[r], x[r2]), hi = umax64(x[r], x[r2]);
+            x[r] = up ? lo : hi;
+            x[r2] = up ? hi : lo;
           }
         }
+      } else if (j < KPT * 32) {
+        const int lm = j / KPT;
+        const bool lower = (t & lm) == 0;
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+          const bool up = ((t * KPT + r) & k) == 0;
+          const uint64_t o = __shfl_xor_sync(kFull, x[r], lm);
+          x[r] = (lower == up) ? umin64(x[r], o) : umax64(x[r], o);
+        }
+      } else {
+        const int tm = j / KPT;
+        const bool lower = (t & tm) == 0;
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) s[r * NT + t] = x[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+          const bool up = ((t * KPT + r) & k) == 0;
+          const uint64_t o = s[r * NT + (t ^ tm)];
+          x[r] = (lower == up) ? umin64(x[r], o) : umax64(x[r], o);
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
 }
 
-__device__ __forceinline__ int pow2_ceil(int x) {
-  int p = 1;
-  while (p < x) p <<= 1;
-  return p;
+template <int KPT>
+__device__ __forceinline__ void sort_block(uint64_t* s, int n, int tid) {
+  uint64_t x[KPT];
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int e = tid * KPT + r;
+    x[r] = e < n ? s[e] : ~0ull;
+  }
+  __syncthreads();
+  bitonic_regs<KPT, kThreads>(x, tid, s);
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int e = tid * KPT + r;
+    if (e < n) s[e] = x[r];
+  }
+  __syncthreads();
 }
 
-template <typename ACC>
-__device__ __forceinline__ ACC warp_sum(ACC v) {
+template <int KPT>
+__device__ __forceinline__ void sort_warp0(uint64_t* s, int n, int tid) {
+  if (tid < 32) {
+    uint64_t x[KPT];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    for (int r = 0; r < KPT; ++r) {
+      const int e = tid * KPT + r;
+      x[r] = e < n ? s[e] : ~0ull;
+    }
+    bitonic_regs<KPT, 32>(x, tid, nullptr);
+#pragma unroll
+    for (int r = 0; r < KPT; ++r) {
+      const int e = tid * KPT + r;
+      if (e < n) s[e] = x[r];
+    }
+  }
+  __syncthreads();
+}
+
+// Sort s[0..n) ascending in place (n <= 4096; block-uniform call).
+__device__ void sort_keys(uint64_t* s, int n, int tid) {
+  if (n <= 1) return;
+  if (n <= 32) return sort_warp0<1>(s, n, tid);
+  if (n <= 64) return sort_warp0<2>(s, n, tid);
+  if (n <= 128) return sort_warp0<4>(s, n, tid);
+  if (n <= 256) return sort_block<1>(s, n, tid);
+  if (n <= 512) return sort_block<2>(s, n, tid);
+  if (n <= 1024) return sort_block<4>(s, n, tid);
+  if (n <= 2048) return sort_block<8>(s, n, tid);
+  return sort_block<16>(s, n, tid);
+}
+
+// out[0..outn) = first outn of merge(A[0..na), B[0..nb)); keys unique.
+// Merge path: each thread owns a contiguous slice of the output.
+__device__ __forceinline__ void merge_path(const uint64_t* A, int na, const uint64_t* B, int nb,
+                                           uint64_t* out, int outn, int tid) {
+  const int per = (outn + kThreads - 1) / kThreads;
+  const int o0 = min(tid * per, outn), o1 = min(o0 + per, outn);
+  if (o0 >= o1) return;
+  int lo = max(0, o0 - nb), hi = min(o0, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] < B[o0 - mid - 1]) lo = mid + 1; else hi = mid;
+  }
+  int ia = lo, ib = o0 - lo;
+  for (int o = o0; o < o1; ++o) {
+    const bool takeA = ib >= nb || (ia < na && A[ia] < B[ib]);
+    out[o] = takeA ? A[ia++] : B[ib++];
+  }
+}
+
+// U partial sums per lane -> lane holds the full sum of vector
+// (lane >> (5 - log2 U)) & (U - 1): log2(U) "transpose" stages that halve the
+// live values, then a plain butterfly (U - 1 + 5 - log2 U shuffles instead of 5U).
+template <int U, typename ACC>
+__device__ __forceinline__ ACC transpose_reduce(ACC (&p)[U], int lane) {
+  constexpr int LU = ilog2(U);
+#pragma unroll
+  for (int st = 0; st < LU; ++st) {
+    const int half = U >> (st + 1);
+    const int off = 16 >> st;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const ACC send = upper ? p[i] : p[i + half];
+      const ACC keep = upper ? p[i + half] : p[i];
+      p[i] = keep + __shfl_xor_sync(kFull, send, off);
+    }
+  }
+  ACC v = p[0];
+#pragma unroll
+  for (int off = 16 >> LU; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
   return v;
 }
 
@@ -188,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
     const PartDesc part = a.parts[a.unit_part[unit]];
     const uint64_t row0 = part.row_off;
     const uint32_t n = part.n;
+    const float* vbase = a.vectors + row0 * (uint64_t)a.dpad;
 
     // query slice in registers: lane holds dims [lane*4 + 128 v, +4)
     float4 q[VPL];
@@ -289,40 +398,49 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
         const int M = st.ncand;
         visited += (uint64_t)M;
 
-        // ---- score new candidates: warp per vector, U in flight
+        // ---- score new candidates: warp per vector, U vectors in flight per warp
         for (int cb = warp * U; cb < M; cb += kWarps * U) {
+          uint32_t ids_u[U];
+          if constexpr (U >= 4) {
+#pragma unroll
+            for (int u4 = 0; u4 < U; u4 += 4) {
+              const uint4 w4 = *reinterpret_cast<const uint4*>(cand + cb + u4);
+              ids_u[u4] = w4.x; ids_u[u4 + 1] = w4.y; ids_u[u4 + 2] = w4.z; ids_u[u4 + 3] = w4.w;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) ids_u[u] = cand[cb + u];
+          }
           float4 x[U][VPL];
-          uint32_t loc[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const int ci = cb + u;
-            loc[u] = ci < M ? cand[ci] : 0u;
-            const float* row = a.vectors + (row0 + loc[u]) * (uint64_t)a.dpad;
+            const bool valid = cb + u < M;
+            const float* row = vbase + (uint64_t)ids_u[u] * (uint64_t)a.dpad;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
               const int b = lane * 4 + 128 * v;
-              if (ci < M && b < a.dpad) x[u][v] = ldg_f4(row + b);
+              if (valid && b < a.dpad) x[u][v] = ldg_f4(row + b);
               else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
-          ACC s[U];
+          ACC part[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             ACC acc = lane_partial<ACC, METRIC>(x[u][0], q[0]);
 #pragma unroll
             for (int v = 1; v < VPL; ++v) acc += lane_partial<ACC, METRIC>(x[u][v], q[v]);
-            s[u] = warp_sum<ACC>(acc);
+            part[u] = acc;
           }
-          // lane u owns result u
-          uint64_t mykey = ~0ull;
+          const ACC tot = transpose_reduce<U, ACC>(part, lane);
+          constexpr int LU = ilog2(U);
+          const int myu = (lane >> (5 - LU)) & (U - 1);
+          const int ci = cb + myu;
           bool pass = false;
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (lane == u && cb + u < M) {
-              const float dist = METRIC == 0 ? (float)s[u] : (float)(-s[u]);
-              mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)loc[u] << 1);
-              pass = mykey < thresh;
-            }
+          uint64_t mykey = 0;
+          if ((lane & ((32 >> LU) - 1)) == 0 && ci < M) {
+            const float dist = METRIC == 0 ? (float)tot : (float)(-tot);
+            mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
+            pass = mykey < thresh;
           }
           const unsigned bal = __ballot_sync(full, pass);
           int base = 0;
@@ -336,20 +454,17 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
         if (S == 0) continue;  // block-uniform
 
         // ---- sort survivors, merge into the pool, truncate at cap
-        const int Sp = pow2_ceil(S);
-        for (int i = S + tid; i < Sp; i += kThreads) surv[i] = ~0ull;
-        __syncthreads();
-        bitonic_sort(surv, Sp);
-        for (int i = tid; i < P; i += kThreads) {
-          const uint64_t key = pool[i];
-          const int pos = i + lower_rank(surv, S, key);
-          if (pos < a.cap) pool_alt[pos] = key;
+#ifdef DVSG_SORT_STATS
+        if (tid == 0 && a.stats) {
+          atomicAdd(a.stats + 3, (unsigned long long)S);
+          atomicAdd(a.stats + 4, (unsigned long long)M);
+          atomicAdd(a.stats + 5, 1ull);
+          atomicAdd(a.stats + 6 + (it < 0 ? 0 : (it < 1 ? 1 : 2)), (unsigned long long)S);
         }
-        for (int j = tid; j < S; j += kThreads) {
-          const uint64_t key = surv[j];
-          const int pos = j + lower_rank(pool, P, key);
-          if (pos < a.cap) pool_alt[pos] = key;
-        }
+#endif
+        sort_keys(surv, S, tid);
+        const int outn = P + S < a.cap ? P + S : a.cap;
+        merge_path(pool, P, surv, S, pool_alt, outn, tid);
         __syncthreads();
         {
           uint64_t* t = pool;
@@ -373,18 +488,13 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
         if ((uint32_t)(pool[mid] >> 32) <= dk) lo = mid + 1; else hi = mid;
       }
       const int m = lo;
-      const int mp = pow2_ceil(m);
-      for (int i = tid; i < mp; i += kThreads) {
-        if (i < m) {
-          const uint64_t key = pool[i];
-          const uint32_t local = (uint32_t)(key >> 1) & 0x7FFFFFFFu;
-          surv[i] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)__ldg(a.gids + row0 + local);
-        } else {
-          surv[i] = ~0ull;
-        }
+      for (int i = tid; i < m; i += kThreads) {
+        const uint64_t key = pool[i];
+        const uint32_t local = (uint32_t)(key >> 1) & 0x7FFFFFFFu;
+        surv[i] = (key & 0xFFFFFFFF00000000ull) | (uint64_t)__ldg(a.gids + row0 + local);
       }
       __syncthreads();
-      bitonic_sort(surv, mp);
+      sort_keys(surv, m, tid);
       for (int i = tid; i < want; i += kThreads) {
         const uint64_t key = surv[i];
         a.out_ids[unit * (uint64_t)a.k + i] = (uint32_t)key;
