@@ -255,7 +255,10 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
 
   static const uint64_t hash_smem_max = [] {
     const char* e = std::getenv("DVSG_HASH_SMEM_MAX");
-    return e ? std::strtoull(e, nullptr, 10) : 16384ull;
+    // default: visited hash in global memory (L2-resident, one 4*hsize-byte
+    // region per persistent CTA).  Measured faster than shared memory at
+    // cfg1 because it frees 64 KB/CTA of smem for occupancy (profiles/).
+    return e ? std::strtoull(e, nullptr, 10) : 0ull;
   }();
   bool in_smem = hsize <= hash_smem_max;
   size_t smem = dvsg::search_smem_bytes((int)cap, (int)chp, p->beam_width, (int)hsize, in_smem);
@@ -296,7 +299,7 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   int max_grid = 0;
   if (!in_smem) {
     // one L2-resident region per persistent CTA
-    max_grid = 4 * c->num_sms;
+    max_grid = 8 * c->num_sms;
     c->hash.reserve((uint64_t)max_grid * hsize, c->stream);
     a.hash_global = c->hash.p;
   }

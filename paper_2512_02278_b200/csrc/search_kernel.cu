@@ -65,7 +65,17 @@ __device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uin
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
-constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+#ifndef DVSG_SORT_ROLLED
+#define DVSG_SORT_ROLLED 1  // measured: rolled stage loops beat full unroll (I-cache)
+#endif
+#ifndef DVSG_SORT_NOINLINE
+#define DVSG_SORT_NOINLINE 0
+#endif
+#ifndef DVSG_SCORE_ROLLED
+#define DVSG_SCORE_ROLLED 0
+#endif
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a < b ? b : a; }
@@ -73,28 +83,44 @@ __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a < 
 // Register-tiled bitonic sort of N = KPT * NT keys, ascending.  Element
 // e = t * KPT + r lives in x[r] of thread t.  Partners closer than KPT are in
 // the same thread (register compare-swap), closer than 32 * KPT in the same
-// warp (shuffles), the rest in other warps: only those log2(NT/32) * (...)
-// stages go through shared memory (r-major, conflict-free) with a barrier.
+// warp (shuffles); only the remaining stages go through shared memory
+// (r-major, conflict-free) with barriers.  Fully unrolled, but sort_keys is
+// __noinline__ so each kernel carries one copy of each network.
+template <int J, int KPT>
+__device__ __forceinline__ void cmpswap_regs(uint64_t (&x)[KPT], int t, int k) {
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int r2 = r ^ J;
+    if (r2 > r) {
+      const bool up = ((t * KPT + r) & k) == 0;
+      const uint64_t lo = umin64(x[r], x[r2]), hi = umax64(x[r], x[r2]);
+      x[r] = up ? lo : hi;
+      x[r2] = up ? hi : lo;
+    }
+  }
+}
+
 template <int KPT, int NT>
 __device__ __forceinline__ void bitonic_regs(uint64_t (&x)[KPT], int t, uint64_t* s) {
   constexpr int LOGN = ilog2(KPT * NT);
+#if DVSG_SORT_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int lk = 1; lk <= LOGN; ++lk) {
     const int k = 1 << lk;
+#if DVSG_SORT_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
     for (int lj = lk - 1; lj >= 0; --lj) {
       const int j = 1 << lj;
       if (j < KPT) {
-#pragma unroll
-        for (int r = 0; r < KPT; ++r) {
-          const int r2 = r ^ j;
-          if (r2 > r) {
-            const bool up = ((t * KPT + r) & k) == 0;
-            const uint64_t lo = umin64(x[r], x[r2]), hi = umax64(x[r], x[r2]);
-            x[r] = up ? lo : hi;
-            x[r2] = up ? hi : lo;
-          }
-        }
+        if (j == 1) cmpswap_regs<1, KPT>(x, t, k);
+        if (KPT > 2 && j == 2) cmpswap_regs<(KPT > 2 ? 2 : 1), KPT>(x, t, k);
+        if (KPT > 4 && j == 4) cmpswap_regs<(KPT > 4 ? 4 : 1), KPT>(x, t, k);
       } else if (j < KPT * 32) {
         const int lm = j / KPT;
         const bool lower = (t & lm) == 0;
@@ -159,8 +185,36 @@ __device__ __forceinline__ void sort_warp0(uint64_t* s, int n, int tid) {
   __syncthreads();
 }
 
-// Sort s[0..n) ascending in place (n <= 4096; block-uniform call).
-__device__ void sort_keys(uint64_t* s, int n, int tid) {
+// Plain shared-memory bitonic for the rare n > 2048 (final sort when cap > 2048).
+__device__ void sort_smem_large(uint64_t* s, int n, int tid) {
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = n + tid; i < np; i += kThreads) s[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int p = tid; p < (np >> 1); p += kThreads) {
+        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+        const int ixj = i | j;
+        const uint64_t a = s[i], b = s[ixj];
+        const bool up = (i & k) == 0;
+        if ((a > b) == up) {
+          s[i] = b;
+          s[ixj] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Sort s[0..n) ascending in place (block-uniform call; s holds >= pow2(n)).
+#if DVSG_SORT_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void sort_keys(uint64_t* s, int n, int tid) {
   if (n <= 1) return;
   if (n <= 32) return sort_warp0<1>(s, n, tid);
   if (n <= 64) return sort_warp0<2>(s, n, tid);
@@ -169,7 +223,7 @@ __device__ void sort_keys(uint64_t* s, int n, int tid) {
   if (n <= 512) return sort_block<2>(s, n, tid);
   if (n <= 1024) return sort_block<4>(s, n, tid);
   if (n <= 2048) return sort_block<8>(s, n, tid);
-  return sort_block<16>(s, n, tid);
+  return sort_smem_large(s, n, tid);
 }
 
 // out[0..outn) = first outn of merge(A[0..na), B[0..nb)); keys unique.
@@ -269,7 +323,10 @@ struct BlockState {
 
 // VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
 template <int VPL, typename ACC, int METRIC>
-__global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a) {
+#ifndef DVSG_MINB
+#define DVSG_MINB 5  // resident CTAs per SM the register budget is cut for (measured sweep)
+#endif
+__global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const SearchArgs a) {
   constexpr int U = VPL >= 8 ? 1 : (8 / VPL);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ BlockState st;
@@ -399,6 +456,9 @@ __global__ void __launch_bounds__(kThreads, 2) search_kernel(const SearchArgs a)
         visited += (uint64_t)M;
 
         // ---- score new candidates: warp per vector, U vectors in flight per warp
+#if DVSG_SCORE_ROLLED
+#pragma unroll 1
+#endif
         for (int cb = warp * U; cb < M; cb += kWarps * U) {
           uint32_t ids_u[U];
           if constexpr (U >= 4) {
