@@ -1,0 +1,187 @@
+// dvs_gpu.cpp -- drop-in replacement of /root/reference/proj/src/graph_index.cpp
+// that runs the reference's search API on the B200 through the C-ABI
+// (include/dvsg.h).  Same header (include/dvs/graph_index.hpp), same
+// signatures, same exceptions; link it instead of graph_index.cpp and every
+// caller -- run_pipeline (simulator.cpp:317-324), cmd_query, and the
+// reference's own unit tests -- searches on the GPU unchanged.
+//
+//   validate(SearchParams)   graph_index.cpp:14-19      host check (same message)
+//   compute_entry_order      graph_index.cpp:21-44      dvsg_compute_entry_order
+//   build_graph              graph_index.cpp:46-103     dvsg_build_graph (GPU K6)
+//   beam_search_stats        graph_index.cpp:105-187    dvsg_load_partition + dvsg_beam_search (K1)
+//   beam_search / visited_count  :189-197               via beam_search_stats
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dvs/errors.hpp"
+#include "dvs/graph_index.hpp"
+#include "dvsg.h"
+
+namespace {
+
+[[noreturn]] void rethrow(dvsg_status st) {
+  const std::string msg = dvsg_last_error();
+  switch (st) {
+    case DVSG_EINVAL: throw std::invalid_argument(msg);
+    case DVSG_EFORMAT: throw dvs::format_error(msg, 0);
+    default: throw dvs::internal_error(msg);
+  }
+}
+
+void check(dvsg_status st) {
+  if (st != DVSG_OK) rethrow(st);
+}
+
+// One context on device 0 for the process.  Every distinct GraphIndex seen
+// is uploaded once as its own resident partition, keyed by its buffers plus a
+// content fingerprint (so a freed-and-reallocated graph at the same address
+// is never mistaken for the old one); run_pipeline's per-cluster calls then
+// hit resident partitions.
+struct Backend {
+  struct Entry {
+    const void* vec;
+    const void* adj;
+    std::size_t n, adj_n;
+    std::uint64_t fp;
+    std::uint32_t cluster;
+  };
+  std::mutex mu;
+  dvsg_ctx* ctx = nullptr;
+  std::vector<Entry> resident;
+
+  dvsg_ctx* get() {
+    if (!ctx) check(dvsg_create(0, &ctx));
+    return ctx;
+  }
+  static std::uint64_t fingerprint(const dvs::GraphIndex& g) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* p, std::size_t bytes) {
+      const unsigned char* c = static_cast<const unsigned char*>(p);
+      for (std::size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    };
+    const std::size_t vb = g.vectors.data.size() * 4, ab = g.adjacency.size() * 4;
+    if (vb + ab <= (64u << 20)) {  // full content for small graphs
+      mix(g.vectors.data.data(), vb);
+      mix(g.adjacency.data(), ab);
+      mix(g.global_ids.data(), g.global_ids.size() * 4);
+    } else {                       // strided sample for large ones
+      for (std::size_t i = 0; i < g.vectors.data.size(); i += 4093) mix(&g.vectors.data[i], 4);
+      for (std::size_t i = 0; i < g.adjacency.size(); i += 4093) mix(&g.adjacency[i], 4);
+    }
+    return h;
+  }
+  std::uint32_t ensure(const dvs::GraphIndex& g) {
+    const std::uint64_t fp = fingerprint(g);
+    for (const Entry& e : resident)
+      if (e.vec == g.vectors.data.data() && e.adj == g.adjacency.data() && e.n == g.size() &&
+          e.adj_n == g.adjacency.size() && e.fp == fp)
+        return e.cluster;
+    int nparts = 0, dim = 0, dg = 0;
+    check(dvsg_index_info(get(), &nparts, &dim, &dg, nullptr, nullptr, nullptr));
+    if (nparts > 0 && (dim != g.vectors.dim || dg != g.out_degree || nparts >= 256)) {
+      check(dvsg_index_reset(ctx));  // shape change or too many graphs: start over
+      resident.clear();
+    }
+    const std::uint32_t cluster = resident.empty() ? 0u : resident.back().cluster + 1u;
+    check(dvsg_load_partition(ctx, cluster, g.size(), g.vectors.dim, g.out_degree,
+                              g.vectors.data.data(), g.adjacency.data(), g.global_ids.data(),
+                              g.entry_order.size() == g.size() ? g.entry_order.data() : nullptr));
+    resident.push_back({g.vectors.data.data(), g.adjacency.data(), g.size(), g.adjacency.size(), fp,
+                        cluster});
+    return cluster;
+  }
+};
+
+Backend& backend() {
+  static Backend b;
+  return b;
+}
+
+}  // namespace
+
+namespace dvs {
+
+void validate(const SearchParams& p) {
+  if (p.iterations < 1 || p.beam_width < 1 || p.k < 1 || p.entry_count < 1) {
+    throw std::invalid_argument(
+        "SearchParams: iterations, beam_width, k and entry_count must all be >= 1");
+  }
+}
+
+std::vector<std::uint32_t> compute_entry_order(const Dataset& partition) {
+  std::vector<std::uint32_t> ids(partition.size());
+  check(dvsg_compute_entry_order(partition.data.data(), partition.size(), partition.dim, ids.data()));
+  return ids;
+}
+
+GraphIndex build_graph(const Dataset& partition, std::vector<std::uint32_t> global_ids,
+                       int out_degree) {
+  validate(partition);
+  const std::size_t n = partition.size();
+  if (n == 0) throw std::invalid_argument("build_graph: empty partition");
+  if (out_degree < 1) throw std::invalid_argument("build_graph: out_degree must be >= 1");
+  if (global_ids.size() != n) {
+    throw std::invalid_argument("build_graph: global id count " + std::to_string(global_ids.size()) +
+                                " != partition size " + std::to_string(n));
+  }
+  GraphIndex g;
+  g.vectors = partition;
+  g.global_ids = std::move(global_ids);
+  g.out_degree = out_degree;
+  g.adjacency.resize(n * static_cast<std::size_t>(out_degree));
+  Backend& b = backend();
+  std::lock_guard<std::mutex> lk(b.mu);
+  check(dvsg_build_graph(b.get(), partition.data.data(), n, partition.dim, out_degree,
+                         g.adjacency.data()));
+  g.entry_order = compute_entry_order(partition);
+  return g;
+}
+
+GraphIndex build_graph(const Dataset& partition, int out_degree) {
+  std::vector<std::uint32_t> ids(partition.size());
+  std::iota(ids.begin(), ids.end(), 0u);
+  return build_graph(partition, std::move(ids), out_degree);
+}
+
+SearchResult beam_search_stats(const GraphIndex& g, std::span<const float> query,
+                               const SearchParams& p, std::uint64_t /*seed*/) {
+  validate(p);
+  if (g.size() == 0) throw std::invalid_argument("beam_search: empty graph");
+  if (static_cast<int>(query.size()) != g.vectors.dim) {
+    throw std::invalid_argument("beam_search: query dim " + std::to_string(query.size()) +
+                                " != index dim " + std::to_string(g.vectors.dim));
+  }
+  Backend& b = backend();
+  std::lock_guard<std::mutex> lk(b.mu);
+  const std::uint32_t cluster = b.ensure(g);
+  dvsg_search_params sp{p.iterations, p.beam_width, p.k, p.entry_count, DVSG_METRIC_L2,
+                        DVSG_ACCUM_F64};
+  std::vector<std::uint32_t> ids(static_cast<std::size_t>(p.k));
+  std::vector<float> dists(static_cast<std::size_t>(p.k));
+  std::uint32_t count = 0;
+  std::uint64_t visited = 0;
+  check(dvsg_beam_search(b.ctx, cluster, query.data(), 1, g.vectors.dim, &sp, ids.data(), dists.data(),
+                         &count, &visited));
+  SearchResult r;
+  r.visited = visited;
+  r.hits.resize(count);
+  for (std::uint32_t i = 0; i < count; ++i) r.hits[i] = {ids[i], dists[i]};
+  return r;
+}
+
+std::vector<ScoredId> beam_search(const GraphIndex& g, std::span<const float> query,
+                                  const SearchParams& p, std::uint64_t seed) {
+  return beam_search_stats(g, query, p, seed).hits;
+}
+
+std::uint64_t visited_count(const GraphIndex& g, std::span<const float> query,
+                            const SearchParams& p) {
+  return beam_search_stats(g, query, p).visited;
+}
+
+}  // namespace dvs
