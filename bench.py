@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cache", default="/tmp/dvsg_bench_cache")
+    ap.add_argument("--mode", choices=["auto", "replica", "sharded"], default="auto",
+                    help="N>1 layout: full index per GPU, or node-sharded vectors with the fused "
+                         "NVLink frontier exchange (auto = sharded when N>1)")
     return ap.parse_args()
 
 
@@ -254,7 +257,11 @@ def workload_config(args, world, rec):
         "entry_count": args.entry, "partitions": 1, "accum": args.accum,
         "recall_at_10": None if rec is None else round(rec, 4),
         "l2": "256 MiB buffer written before every timed step",
-        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        "parallelism": (f"node-sharded x{world}: vectors split by id range, adjacency replicated, "
+                        "fused NVLink peer-store frontier exchange" if getattr(args, "_sharded", False)
+                        else (f"replicas x{world}" if world > 1 else "single GPU")),
+        "step": ("K1 sharded search (ids + dists)" if getattr(args, "_sharded", False)
+                 else "run_pipeline: assign + route + K1 + combine + hit vectors"),
     }
 
 
@@ -276,9 +283,20 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    mode = args.mode
+    if mode == "auto":
+        mode = "sharded" if world > 1 else "replica"
+    sharded = mode == "sharded"
+    args._sharded = sharded
+
     ctx = dvs.Context(local)
     data, queries, index = workload(args, rank, ctx)
-    ctx.load_index(index)
+    g0 = index.graphs[0]
+    if sharded:
+        from paper_2512_02278_b200.dist import prepare_step, setup_sharded
+        setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
+    else:
+        ctx.load_index(index)
     p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
     nq, dim, k = args.nq, args.dim, args.k
     dev = torch.device("cuda", local)
@@ -289,17 +307,27 @@ def main():
     d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
     d_counts = torch.empty((nq,), dtype=torch.int32, device=dev)
     d_vecs = torch.empty((nq, k, dim), dtype=torch.float32, device=dev)
+    d_vis = torch.empty((nq,), dtype=torch.int64, device=dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     torch.cuda.synchronize()
 
+    def pre_step():  # untimed: the sharded arenas must be reset on every rank first
+        if sharded:
+            prepare_step(ctx, dist.barrier if dist else (lambda: None))
+
     def step():
-        ctx.run_pipeline_device(d_q.data_ptr(), nq, dim, p, 1, d_ids.data_ptr(), d_dists.data_ptr(),
-                                d_counts.data_ptr(), d_vecs.data_ptr())
+        if sharded:
+            ctx.search_sharded_device(d_q.data_ptr(), nq, dim, p, d_ids.data_ptr(),
+                                      d_dists.data_ptr(), d_counts.data_ptr(), d_vis.data_ptr())
+        else:
+            ctx.run_pipeline_device(d_q.data_ptr(), nq, dim, p, 1, d_ids.data_ptr(),
+                                    d_dists.data_ptr(), d_counts.data_ptr(), d_vecs.data_ptr())
 
     ctx.set_timing(True)
     for _ in range(args.warmup):
+        pre_step()
         step()
-    ctx.synchronize()
+        ctx.synchronize()
 
     # ---- timed region: K steps, L2 flushed before each -------------------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -313,6 +341,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))
             torch.cuda.synchronize()
+            pre_step()
             starts[i].record(stream)
             step()
             ends[i].record(stream)
@@ -334,13 +363,53 @@ def main():
     ids_h = d_ids.cpu().numpy().view(np.uint32)
     cnt_h = d_counts.cpu().numpy().view(np.uint32)
     rec = None
+    shard_parity = None
     if rank == 0:
         s = min(args.recall_sample, nq)
         rec = recall(data, queries[:s], ids_h[:s], cnt_h[:s], k)
+        if sharded:  # the sharded traversal must equal the unsharded one exactly
+            ref_ctx = dvs.Context(local)
+            ref_ctx.load_index(index)
+            ri, rd, rc, rv = ref_ctx.beam_search(0, queries[:s], p)
+            vis_h = d_vis.cpu().numpy()[:s]
+            shard_parity = {"queries": s,
+                            "ids_identical": bool(np.array_equal(ri, ids_h[:s]) and np.array_equal(rc, cnt_h[:s])),
+                            "visited_identical": bool(np.array_equal(rv.astype(np.int64), vis_h))}
+            ref_ctx.close()
 
     # ---- e2e through the public host-buffer call ------------------------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and sharded:
+        # host queries in (pinned H2D), sharded search, ids/dists/counts out (D2H)
+        hq = torch.from_numpy(queries).pin_memory()
+        h_ids = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)
+        h_dists = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
+        h_counts = torch.empty((nq,), dtype=torch.int32, pin_memory=True)
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            pre_step()
+            with torch.cuda.stream(stream):
+                ev0[i].record(stream)
+                d_q.copy_(hq, non_blocking=True)
+                step()
+                h_ids.copy_(d_ids, non_blocking=True)
+                h_dists.copy_(d_dists, non_blocking=True)
+                h_counts.copy_(d_counts, non_blocking=True)
+                ev1[i].record(stream)
+            stream.synchronize()
+        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        assert np.array_equal(h_ids.numpy().view(np.uint32), ids_h), "e2e and device paths disagree"
+        e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(hq.numel() * 4),
+               "d2h_bytes_per_step": int((h_ids.numel() + h_dists.numel() + h_counts.numel()) * 4),
+               "ms_per_step": float(e_ms[0]) / args.steps,
+               "note": "sharded mode returns ids + dists (hit vectors stay on their owner GPUs)"}
+    elif not args.no_e2e:
         keep = []
 
         def pin(shape, dt):
@@ -424,6 +493,7 @@ def main():
                      "visited_per_query": vis_tot / max(units_tot, 1),
                      "expanded_per_query": exp_tot / max(units_tot, 1)},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "sharded_parity_vs_unsharded": shard_parity,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -128,6 +128,41 @@ dvsg_status dvsg_search_units_device(dvsg_ctx *ctx, const float *d_queries, uint
                                      float *d_out_dists, uint32_t *d_out_count,
                                      uint64_t *d_out_visited);
 
+/* ---- node-sharded search (north-star frontier exchange) -----------------
+ * The graph's vectors are split across ranks (node v on rank v / ceil(n/R));
+ * adjacency, global ids and entry order are replicated.  One fused kernel per
+ * GPU: the origin keeps pool + visited set, pushes remote candidate ids (and
+ * the query) to their owners by NVLink peer stores, owners score against
+ * their rows and push keys back; results are identical to the unsharded
+ * beam_search_stats (graph_index.cpp:105-187). */
+
+/* All R ranks emulated in one launch on this device over the resident
+ * whole-graph partition (for parity tests without R GPUs).  Host buffers. */
+dvsg_status dvsg_beam_search_sharded_emulated(dvsg_ctx *ctx, int nranks, const float *queries,
+                                              uint64_t nq, int dim, const dvsg_search_params *p,
+                                              uint32_t *out_ids, float *out_dists,
+                                              uint32_t *out_count, uint64_t *out_visited);
+/* Multi-GPU, one process per GPU: load this rank's shard rows
+ * [rank*S, min(n,(rank+1)*S)) with S = ceil(n_total/nranks) plus the
+ * replicated adjacency / global ids (NULL = iota) / entry order (required,
+ * graph_index.cpp:21-44 over the whole graph); allocates the comm arena. */
+dvsg_status dvsg_shard_init(dvsg_ctx *ctx, int nranks, int rank, uint64_t n_total, int dim,
+                            int out_degree, const float *shard_vectors, const uint32_t *adjacency,
+                            const uint32_t *global_ids, const uint32_t *entry_order);
+/* 64-byte IPC handle of this rank's comm arena (exchange it across ranks). */
+dvsg_status dvsg_shard_export(dvsg_ctx *ctx, void *handle_out);
+/* Open every rank's arena (handles: nranks x 64 bytes, in rank order). */
+dvsg_status dvsg_shard_connect(dvsg_ctx *ctx, const void *handles);
+/* Reset this rank's arena before a search; all ranks must finish it (host
+ * barrier) before any rank launches. */
+dvsg_status dvsg_shard_prepare(dvsg_ctx *ctx);
+/* Sharded search of this rank's nq queries (device pointers, async on the
+ * compute stream); every rank must launch it concurrently. */
+dvsg_status dvsg_search_sharded_device(dvsg_ctx *ctx, const float *d_queries, uint64_t nq, int dim,
+                                       const dvsg_search_params *p, uint32_t *d_out_ids,
+                                       float *d_out_dists, uint32_t *d_out_count,
+                                       uint64_t *d_out_visited);
+
 /* ---- routing and merge -------------------------------------------------- */
 
 /* assign_top_c, kmeans.cpp:243-280, on the GPU against the context's

@@ -58,6 +58,15 @@ _SIGS = {
     "dvsg_search_units_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_void_p,
                                          c_uint64, P_params, c_void_p, c_void_p, c_void_p,
                                          c_void_p]),
+    "dvsg_beam_search_sharded_emulated": (c_int, [c_void_p, c_int, c_void_p, c_uint64, c_int, P_params,
+                                                  c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dvsg_shard_init": (c_int, [c_void_p, c_int, c_int, c_uint64, c_int, c_int, c_void_p, c_void_p,
+                                c_void_p, c_void_p]),
+    "dvsg_shard_export": (c_int, [c_void_p, c_void_p]),
+    "dvsg_shard_connect": (c_int, [c_void_p, c_void_p]),
+    "dvsg_shard_prepare": (c_int, [c_void_p]),
+    "dvsg_search_sharded_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, P_params, c_void_p,
+                                           c_void_p, c_void_p, c_void_p]),
     "dvsg_assign_top_c": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
     "dvsg_combine_results": (c_int, [c_void_p, c_uint64, c_int, c_void_p, c_void_p, c_void_p,
                                      c_int, c_int, c_void_p, c_void_p, c_void_p]),

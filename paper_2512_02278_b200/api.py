@@ -247,6 +247,54 @@ class Context:
                                    _ptr(ids), _ptr(dists), _ptr(counts), _ptr(visited)))
         return ids, dists, counts, visited
 
+    def beam_search_sharded_emulated(self, nranks: int, queries, p: SearchParams):
+        """Node-sharded search with `nranks` ranks emulated on this device over
+        the resident whole-graph partition -> (ids, dists, counts, visited)."""
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        nq, dim = q.shape
+        cp = p.to_c()
+        k = max(int(p.k), 1)
+        ids = np.zeros((nq, k), np.uint32)
+        dists = np.zeros((nq, k), np.float32)
+        counts = np.zeros(nq, np.uint32)
+        visited = np.zeros(nq, np.uint64)
+        check(lib.dvsg_beam_search_sharded_emulated(self._h, int(nranks), _ptr(q), nq, dim, ctypes.byref(cp),
+                                                    _ptr(ids), _ptr(dists), _ptr(counts), _ptr(visited)))
+        return ids, dists, counts, visited
+
+    # ---- node-sharded multi-GPU (one process per GPU) --------------------------
+    def shard_init(self, nranks: int, rank: int, shard_vectors, n_total: int, adjacency,
+                   entry_order, global_ids=None) -> None:
+        v = _f32(shard_vectors, 2)
+        adj = _u32(adjacency)
+        eo = _u32(entry_order)
+        gids = None if global_ids is None else _u32(global_ids)
+        check(lib.dvsg_shard_init(self._h, int(nranks), int(rank), int(n_total), v.shape[1],
+                                  int(adj.shape[1]), _ptr(v), _ptr(adj), _ptr(gids), _ptr(eo)))
+
+    def shard_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        check(lib.dvsg_shard_export(self._h, buf))
+        return buf.raw
+
+    def shard_connect(self, handles) -> None:
+        blob = b"".join(handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        check(lib.dvsg_shard_connect(self._h, buf))
+
+    def shard_prepare(self) -> None:
+        check(lib.dvsg_shard_prepare(self._h))
+
+    def search_sharded_device(self, d_queries: int, nq: int, dim: int, p: SearchParams, d_ids: int,
+                              d_dists: int, d_counts: int, d_visited: int) -> None:
+        cp = p.to_c()
+        check(lib.dvsg_search_sharded_device(self._h, ctypes.c_void_p(d_queries), int(nq), int(dim),
+                                             ctypes.byref(cp), ctypes.c_void_p(d_ids),
+                                             ctypes.c_void_p(d_dists), ctypes.c_void_p(d_counts),
+                                             ctypes.c_void_p(d_visited)))
+
     def assign_top_c(self, queries, c: int) -> np.ndarray:
         q = _f32(queries, 2)
         out = np.zeros((q.shape[0], max(int(c), 1)), np.uint32)

@@ -44,6 +44,48 @@ struct SearchArgs {
   unsigned long long* stats;  // [0] units, [1] visited, [2] expanded (frontier nodes); nullable
 };
 
+// ---- node-sharded K1 (shard_kernel.cu) ------------------------------------
+// Vectors of node v live on rank v / shard_rows; adjacency, global ids and
+// entry order are replicated.  Each rank's comm arena holds its doorbell ring,
+// the mailboxes peers push candidate ids + query into, the reply boxes peers
+// push scored keys into, and counters.  `views` gives every rank's arena (peer
+// pointers over NVLink, or slices of one device when emulating ranks).
+struct ShardView {
+  const float* vec;              // this rank's shard rows (dpad floats each)
+  uint32_t* ring;                // doorbell ring [ring_mask + 1], entries (origin<<16 | cta) + 1
+  unsigned* ring_tail;           // producers reserve slots (peer atomics)
+  unsigned* ring_head;           // local consumers claim slots
+  unsigned char* mail;           // [nranks * gpr] mailboxes, mail_stride bytes each
+  unsigned char* reply;          // [gpr * nranks] reply boxes, reply_stride bytes each
+  unsigned* done;                // ranks that finished all their units
+  unsigned* finished;            // CTAs of this rank that finished their units
+  unsigned long long* work;      // this rank's unit counter
+};
+
+struct ShardArgs {
+  const ShardView* views;        // device array [nranks]
+  int nranks;
+  int rank_self;                 // >= 0: one rank per launch (multi-GPU); -1: emulate all ranks
+  int gpr;                       // CTAs per rank
+  uint64_t shard_rows;           // S
+  uint32_t ring_mask;
+  uint32_t mail_stride;
+  uint32_t reply_stride;
+  uint64_t units_per_rank;       // emulation: rank r owns units [r*upr, (r+1)*upr)
+};
+
+// Comm-arena layout helpers (bytes), shared by host and device.
+__host__ __device__ inline uint32_t shard_mail_stride(int dpad) {
+  return (uint32_t)(16 + 4 * dpad + 4 * 2048 + 15) & ~15u;
+}
+__host__ __device__ inline uint32_t shard_reply_stride() { return 16 + 8 * 2048; }
+
+cudaError_t launch_search_sharded(const SearchArgs& a, const ShardArgs& sh, int metric, int accum,
+                                  int num_sms, cudaStream_t stream, int* grid_out,
+                                  int* gpr_out);
+// CTAs per rank the sharded kernel can keep resident for these args.
+int search_sharded_blocks_per_sm(const SearchArgs& a, int metric, int accum);
+
 // Launch K1 (search_kernel.cu).  Returns a cudaError_t.
 // max_grid > 0 caps the persistent grid (one global hash region per CTA).
 cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sms,

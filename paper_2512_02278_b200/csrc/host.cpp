@@ -142,6 +142,22 @@ struct dvsg_ctx {
   DevBuf<float> io_f, io_dists, io_vecs;
   DevBuf<uint32_t> io_u;
   DevBuf<uint64_t> io_u64;
+  // node-sharded mode (shard_kernel.cu)
+  struct Shard {
+    bool active = false;     // ctx holds one rank's shard (multi-GPU)
+    int nranks = 0, rank = 0;
+    uint64_t n_total = 0, shard_rows = 0;
+    int gpr_max = 0;
+    uint32_t ring_cap = 0;
+    size_t arena_bytes = 0;
+    unsigned char* arena = nullptr;            // own comm arena (IPC-exported)
+    std::vector<unsigned char*> peers;         // every rank's arena (own included)
+    bool connected = false;
+  } sh;
+  DevBuf<unsigned char> emu_arena;             // emulation: all virtual ranks' arenas
+  DevBuf<dvsg::ShardView> d_views;
+  DevBuf<uint32_t> iota_q, zero_p;
+  uint64_t iota_n = 0;
   // timing
   bool timing = false;
   cudaEvent_t ev[8] = {};
@@ -233,26 +249,22 @@ uint64_t pow2_at_least(uint64_t x) {
   return p;
 }
 
-// Core: K1 over a device unit list.  All pointers device.
-void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uint32_t* d_uq,
-                  const uint32_t* d_up, uint64_t nunits, const dvsg_search_params* p,
-                  uint32_t* d_ids, float* d_dists, uint32_t* d_count, uint64_t* d_visited) {
-  validate_params(p);
-  if (c->parts.empty()) fail(DVSG_EINVAL, "beam_search: empty graph");
-  if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
-  if (nunits == 0) return;
-  if ((uint64_t)p->beam_width * (uint64_t)c->dg > (1ull << 30)) fail(DVSG_EINVAL, "beam_search: beam_width * out_degree too large");
-  sync_parts(c);
-  const uint64_t cap = std::max<uint64_t>(4ull * (uint64_t)p->k, 2ull * (uint64_t)p->iterations * (uint64_t)p->beam_width);
-  if (cap > (1ull << 20)) fail(DVSG_EINVAL, "beam_search: candidate pool capacity %llu exceeds the device limit", (unsigned long long)cap);
+// Shapes of a K1 launch for these params (cap, survivor buffer, hash size).
+struct K1Shape {
+  uint64_t cap, chp, hsize;
+  bool hash_in_smem;
+  size_t smem;
+};
+
+K1Shape k1_shape(dvsg_ctx* c, const dvsg_search_params* p, uint64_t nmax, bool allow_smem_hash) {
+  K1Shape k{};
+  k.cap = std::max<uint64_t>(4ull * (uint64_t)p->k, 2ull * (uint64_t)p->iterations * (uint64_t)p->beam_width);
+  if (k.cap > (1ull << 20)) fail(DVSG_EINVAL, "beam_search: candidate pool capacity %llu exceeds the device limit", (unsigned long long)k.cap);
   // visited never exceeds min(n_max, entries + I*w*dg)
-  uint64_t nmax = 0;
-  for (auto& pd : c->parts) nmax = std::max<uint64_t>(nmax, pd.n);
   const uint64_t entries = std::min<uint64_t>((uint64_t)p->entry_count, nmax);
   const uint64_t bound = std::min<uint64_t>(nmax, entries + (uint64_t)p->iterations * (uint64_t)p->beam_width * (uint64_t)c->dg);
-  const uint64_t hsize = std::max<uint64_t>(64, pow2_at_least(bound + 1));
-  const uint64_t chp = std::max<uint64_t>(pow2_at_least((uint64_t)dvsg::kChunk), pow2_at_least(cap));
-
+  k.hsize = std::max<uint64_t>(64, pow2_at_least(bound + 1));
+  k.chp = std::max<uint64_t>(pow2_at_least((uint64_t)dvsg::kChunk), pow2_at_least(k.cap));
   static const uint64_t hash_smem_max = [] {
     const char* e = std::getenv("DVSG_HASH_SMEM_MAX");
     // default: visited hash in global memory (L2-resident, one 4*hsize-byte
@@ -260,12 +272,18 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
     // cfg1 because it frees 64 KB/CTA of smem for occupancy (profiles/).
     return e ? std::strtoull(e, nullptr, 10) : 0ull;
   }();
-  bool in_smem = hsize <= hash_smem_max;
-  size_t smem = dvsg::search_smem_bytes((int)cap, (int)chp, p->beam_width, (int)hsize, in_smem);
-  if (in_smem && smem > c->smem_optin) in_smem = false;
-  smem = dvsg::search_smem_bytes((int)cap, (int)chp, p->beam_width, (int)hsize, in_smem);
-  if (smem > c->smem_optin) fail(DVSG_EINVAL, "beam_search: pool (%llu) too large for shared memory", (unsigned long long)cap);
+  k.hash_in_smem = allow_smem_hash && k.hsize <= hash_smem_max;
+  k.smem = dvsg::search_smem_bytes((int)k.cap, (int)k.chp, p->beam_width, (int)k.hsize, k.hash_in_smem);
+  if (k.hash_in_smem && k.smem > c->smem_optin) k.hash_in_smem = false;
+  k.smem = dvsg::search_smem_bytes((int)k.cap, (int)k.chp, p->beam_width, (int)k.hsize, k.hash_in_smem);
+  if (k.smem > c->smem_optin) fail(DVSG_EINVAL, "beam_search: pool (%llu) too large for shared memory", (unsigned long long)k.cap);
+  return k;
+}
 
+dvsg::SearchArgs k1_args(dvsg_ctx* c, const dvsg_search_params* p, const K1Shape& k, const float* d_q,
+                         uint64_t nq, int dim, const uint32_t* d_uq, const uint32_t* d_up,
+                         uint64_t nunits, uint32_t* d_ids, float* d_dists, uint32_t* d_count,
+                         uint64_t* d_visited) {
   dvsg::SearchArgs a{};
   a.vectors = c->vec.p;
   a.adjacency = c->adj.p;
@@ -284,9 +302,9 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   a.beam = p->beam_width;
   a.k = p->k;
   a.entry_count = p->entry_count;
-  a.cap = (int)cap;
-  a.chp = (int)chp;
-  a.hsize = (int)hsize;
+  a.cap = (int)k.cap;
+  a.chp = (int)k.chp;
+  a.hsize = (int)k.hsize;
   a.out_ids = d_ids;
   a.out_dists = d_dists;
   a.out_count = d_count;
@@ -296,16 +314,146 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   a.stats = c->counter.p + 1;
   cuda_check(cudaMemsetAsync(c->counter.p, 0, 16 * sizeof(unsigned long long), c->stream), "counter reset");
   c->stats_pending = true;
+  return a;
+}
+
+// Core: K1 over a device unit list.  All pointers device.
+void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uint32_t* d_uq,
+                  const uint32_t* d_up, uint64_t nunits, const dvsg_search_params* p,
+                  uint32_t* d_ids, float* d_dists, uint32_t* d_count, uint64_t* d_visited) {
+  validate_params(p);
+  if (c->sh.active) fail(DVSG_EINVAL, "beam_search: this context holds one rank's shard; use dvsg_search_sharded_device");
+  if (c->parts.empty()) fail(DVSG_EINVAL, "beam_search: empty graph");
+  if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
+  if (nunits == 0) return;
+  if ((uint64_t)p->beam_width * (uint64_t)c->dg > (1ull << 30)) fail(DVSG_EINVAL, "beam_search: beam_width * out_degree too large");
+  sync_parts(c);
+  uint64_t nmax = 0;
+  for (auto& pd : c->parts) nmax = std::max<uint64_t>(nmax, pd.n);
+  const K1Shape k = k1_shape(c, p, nmax, true);
+  dvsg::SearchArgs a = k1_args(c, p, k, d_q, nq, dim, d_uq, d_up, nunits, d_ids, d_dists, d_count, d_visited);
   int max_grid = 0;
-  if (!in_smem) {
+  if (!k.hash_in_smem) {
     // one L2-resident region per persistent CTA
     max_grid = 8 * c->num_sms;
-    c->hash.reserve((uint64_t)max_grid * hsize, c->stream);
+    c->hash.reserve((uint64_t)max_grid * k.hsize, c->stream);
     a.hash_global = c->hash.p;
   }
   if (c->timing) cudaEventRecord(c->ev[0], c->stream);
   int grid = 0;
   cuda_check(dvsg::launch_search(a, p->metric, p->accum, c->num_sms, max_grid, c->stream, &grid), "search kernel launch");
+  if (c->timing) {
+    cudaEventRecord(c->ev[1], c->stream);
+    c->timing_pending = 1;
+  }
+  c->launches += 1;
+}
+
+// ---- node-sharded search --------------------------------------------------
+constexpr size_t kArenaHeader = 256;  // work u64 @0, done @8, finished @12, ring_head @16, ring_tail @20
+
+size_t shard_arena_bytes(int nranks, int gpr_max, uint32_t ring_cap, int dpad) {
+  size_t b = kArenaHeader + (size_t)ring_cap * 4;
+  b = (b + 255) & ~(size_t)255;
+  b += (size_t)nranks * gpr_max * dvsg::shard_mail_stride(dpad);
+  b = (b + 255) & ~(size_t)255;
+  b += (size_t)gpr_max * nranks * dvsg::shard_reply_stride();
+  return b;
+}
+
+dvsg::ShardView shard_view(unsigned char* arena, const float* vec, int nranks, int gpr_max,
+                           uint32_t ring_cap, int dpad) {
+  dvsg::ShardView v{};
+  v.vec = vec;
+  v.work = reinterpret_cast<unsigned long long*>(arena);
+  v.done = reinterpret_cast<unsigned*>(arena + 8);
+  v.finished = reinterpret_cast<unsigned*>(arena + 12);
+  v.ring_head = reinterpret_cast<unsigned*>(arena + 16);
+  v.ring_tail = reinterpret_cast<unsigned*>(arena + 20);
+  v.ring = reinterpret_cast<uint32_t*>(arena + kArenaHeader);
+  size_t off = (kArenaHeader + (size_t)ring_cap * 4 + 255) & ~(size_t)255;
+  v.mail = arena + off;
+  off += (size_t)nranks * gpr_max * dvsg::shard_mail_stride(dpad);
+  off = (off + 255) & ~(size_t)255;
+  v.reply = arena + off;
+  return v;
+}
+
+const uint32_t* iota_units(dvsg_ctx* c, uint64_t n, const uint32_t** zero_parts) {
+  if (c->iota_n < n) {
+    std::vector<uint32_t> h(n);
+    std::iota(h.begin(), h.end(), 0u);
+    c->iota_q.reserve(n, c->stream);
+    c->zero_p.reserve(n, c->stream);
+    cuda_check(cudaMemcpyAsync(c->iota_q.p, h.data(), n * 4, cudaMemcpyHostToDevice, c->stream), "iota");
+    cuda_check(cudaMemsetAsync(c->zero_p.p, 0, n * 4, c->stream), "zero");
+    cuda_check(cudaStreamSynchronize(c->stream), "iota");
+    c->iota_n = n;
+  }
+  *zero_parts = c->zero_p.p;
+  return c->iota_q.p;
+}
+
+// Launch the sharded kernel.  emulate: all ranks in one launch on this device.
+void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64_t nq, int dim,
+                    const dvsg_search_params* p, uint32_t* d_ids, float* d_dists, uint32_t* d_count,
+                    uint64_t* d_visited) {
+  validate_params(p);
+  if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
+  if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
+  if (nranks < 1 || nranks > 8) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
+  if (c->dpad > 768) fail(DVSG_EINVAL, "sharded search: dim above 768 not supported");
+  if (nq == 0) return;
+  sync_parts(c);
+  const uint64_t n = c->sh.active ? c->sh.n_total : c->parts[0].n;
+  const K1Shape k = k1_shape(c, p, n, false);
+  const uint32_t* zp = nullptr;
+  const uint32_t* uq = iota_units(c, nq, &zp);
+  dvsg::SearchArgs a = k1_args(c, p, k, d_q, nq, dim, uq, zp, nq, d_ids, d_dists, d_count, d_visited);
+  const int per_sm = dvsg::search_sharded_blocks_per_sm(a, p->metric, p->accum);
+  if (per_sm < 1) fail(DVSG_EINTERNAL, "sharded search: kernel does not fit on an SM");
+  const int resident = per_sm * c->num_sms;
+  const int gpr_max = 8 * c->num_sms;
+  const uint32_t ring_cap = (uint32_t)pow2_at_least((uint64_t)nranks * gpr_max);
+  dvsg::ShardArgs sh{};
+  sh.nranks = nranks;
+  sh.ring_mask = ring_cap - 1;
+  sh.mail_stride = dvsg::shard_mail_stride(c->dpad);
+  sh.reply_stride = dvsg::shard_reply_stride();
+  std::vector<dvsg::ShardView> views((size_t)nranks);
+  if (emulate) {
+    sh.rank_self = -1;
+    sh.gpr = resident / nranks;
+    sh.shard_rows = (n + (uint64_t)nranks - 1) / (uint64_t)nranks;
+    sh.units_per_rank = (nq + (uint64_t)nranks - 1) / (uint64_t)nranks;
+    const size_t ab = shard_arena_bytes(nranks, sh.gpr, ring_cap, c->dpad);
+    c->emu_arena.reserve(ab * (size_t)nranks, c->stream);
+    cuda_check(cudaMemsetAsync(c->emu_arena.p, 0, ab * (size_t)nranks, c->stream), "arena reset");
+    for (int r = 0; r < nranks; ++r)
+      views[(size_t)r] = shard_view(c->emu_arena.p + ab * (size_t)r,
+                                    c->vec.p + (uint64_t)r * sh.shard_rows * (uint64_t)c->dpad,
+                                    nranks, sh.gpr, ring_cap, c->dpad);
+  } else {
+    if (!c->sh.active || !c->sh.connected) fail(DVSG_EINVAL, "sharded search: call dvsg_shard_init and dvsg_shard_connect first");
+    if (nranks != c->sh.nranks) fail(DVSG_EINVAL, "sharded search: nranks %d != %d", nranks, c->sh.nranks);
+    sh.rank_self = c->sh.rank;
+    sh.gpr = std::min(resident, c->sh.gpr_max);
+    sh.shard_rows = c->sh.shard_rows;
+    sh.units_per_rank = nq;
+    for (int r = 0; r < nranks; ++r)
+      views[(size_t)r] = shard_view(c->sh.peers[(size_t)r], r == c->sh.rank ? c->vec.p : nullptr,
+                                    nranks, c->sh.gpr_max, c->sh.ring_cap, c->dpad);
+    sh.ring_mask = c->sh.ring_cap - 1;
+  }
+  c->d_views.reserve((size_t)nranks, c->stream);
+  cuda_check(cudaMemcpyAsync(c->d_views.p, views.data(), views.size() * sizeof(dvsg::ShardView), cudaMemcpyHostToDevice, c->stream), "views");
+  sh.views = c->d_views.p;
+  const int grid_total = emulate ? sh.gpr * nranks : sh.gpr;
+  c->hash.reserve((uint64_t)grid_total * k.hsize, c->stream);
+  a.hash_global = c->hash.p;
+  if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+  int grid = 0, gpr = 0;
+  cuda_check(dvsg::launch_search_sharded(a, sh, p->metric, p->accum, c->num_sms, c->stream, &grid, &gpr), "sharded search launch");
   if (c->timing) {
     cudaEventRecord(c->ev[1], c->stream);
     c->timing_pending = 1;
@@ -503,6 +651,9 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    for (size_t r = 0; r < c->sh.peers.size(); ++r)
+      if ((int)r != c->sh.rank && c->sh.peers[r]) cudaIpcCloseMemHandle(c->sh.peers[r]);
+    if (c->sh.arena) cudaFree(c->sh.arena);
     for (auto& e : c->ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm);
@@ -527,6 +678,8 @@ dvsg_status dvsg_index_reset(dvsg_ctx* c) {
     c->rows = 0;
     c->dim = c->dpad = c->dg = 0;
     c->clusters = 0;
+    c->sh.active = false;
+    c->sh.connected = false;
     c->cents.clear();
     c->placement.clear();
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
@@ -696,6 +849,138 @@ dvsg_status dvsg_search_units_device(dvsg_ctx* c, const float* d_queries, uint64
     cuda_check(dvsg::launch_route(d_unit_cluster, nunits, 1, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
     c->launches += 1;
     search_units(c, d_queries, nq, dim, d_unit_query, c->unit_p.p, nunits, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
+  });
+}
+
+dvsg_status dvsg_beam_search_sharded_emulated(dvsg_ctx* c, int nranks, const float* queries, uint64_t nq,
+                                              int dim, const dvsg_search_params* p, uint32_t* out_ids,
+                                              float* out_dists, uint32_t* out_count, uint64_t* out_visited) {
+  return guarded([&] {
+    set_device(c);
+    validate_params(p);
+    if (c->sh.active) fail(DVSG_EINVAL, "emulated sharded search needs the whole graph resident");
+    if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
+    if (nq == 0) return;
+    if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
+    const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
+    const uint64_t k = (uint64_t)p->k;
+    c->u_ids.reserve(nq * k, c->stream);
+    c->u_dists.reserve(nq * k, c->stream);
+    c->u_count.reserve(nq, c->stream);
+    c->u_visited.reserve(nq, c->stream);
+    search_sharded(c, true, nranks, d_q, nq, dim, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
+    cuda_check(cudaMemcpyAsync(out_ids, c->u_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_dists, c->u_dists.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_count, c->u_count.p, nq * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(out_visited, c->u_visited.p, nq * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "sharded search");
+    read_timings(c, false);
+  });
+}
+
+dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total, int dim, int out_degree,
+                            const float* shard_vectors, const uint32_t* adjacency,
+                            const uint32_t* global_ids, const uint32_t* entry_order) {
+  return guarded([&] {
+    set_device(c);
+    if (nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) fail(DVSG_EINVAL, "shard_init: rank %d of %d", rank, nranks);
+    if (n_total == 0 || n_total >= (1ull << 31)) fail(DVSG_EINVAL, "shard_init: n %llu outside 1..2^31", (unsigned long long)n_total);
+    if (dim < 1 || dim > 768) fail(DVSG_EINVAL, "shard_init: dim %d outside 1..768", dim);
+    if (out_degree < 1) fail(DVSG_EINVAL, "build_graph: out_degree must be >= 1");
+    if (!shard_vectors || !adjacency || !entry_order) fail(DVSG_EINVAL, "shard_init: null input");
+    const uint64_t S = (n_total + (uint64_t)nranks - 1) / (uint64_t)nranks;
+    const uint64_t lo = std::min<uint64_t>(n_total, S * (uint64_t)rank);
+    const uint64_t hi = std::min<uint64_t>(n_total, lo + S);
+    for (uint64_t i = 0; i < n_total * (uint64_t)out_degree; ++i)
+      if (adjacency[i] >= n_total) fail(DVSG_EFORMAT, "index file: neighbor id out of range");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    c->parts.clear();
+    c->dim = dim;
+    c->dpad = (dim + 3) & ~3;
+    c->dg = out_degree;
+    c->rows = n_total;
+    // own shard rows only (at least one row so the buffer exists)
+    const uint64_t rows = std::max<uint64_t>(hi - lo, 1);
+    c->vec.reserve(rows * (uint64_t)c->dpad, c->stream);
+    cuda_check(cudaMemset(c->vec.p, 0, rows * (uint64_t)c->dpad * 4), "memset");
+    if (hi > lo)
+      cuda_check(cudaMemcpy2D(c->vec.p, (size_t)c->dpad * 4, shard_vectors, (size_t)dim * 4, (size_t)dim * 4, hi - lo, cudaMemcpyHostToDevice), "shard H2D");
+    c->adj.reserve(n_total * (uint64_t)out_degree, c->stream);
+    c->gids.reserve(n_total, c->stream);
+    c->entry.reserve(n_total, c->stream);
+    cuda_check(cudaMemcpy(c->adj.p, adjacency, n_total * (uint64_t)out_degree * 4, cudaMemcpyHostToDevice), "adjacency H2D");
+    if (global_ids) {
+      cuda_check(cudaMemcpy(c->gids.p, global_ids, n_total * 4, cudaMemcpyHostToDevice), "gids H2D");
+    } else {
+      std::vector<uint32_t> io(n_total);
+      std::iota(io.begin(), io.end(), 0u);
+      cuda_check(cudaMemcpy(c->gids.p, io.data(), n_total * 4, cudaMemcpyHostToDevice), "gids H2D");
+    }
+    cuda_check(cudaMemcpy(c->entry.p, entry_order, n_total * 4, cudaMemcpyHostToDevice), "entry H2D");
+    c->parts.push_back(dvsg::PartDesc{0, (uint32_t)n_total, 0});
+    c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
+    auto& sh = c->sh;
+    if (sh.arena) cudaFree(sh.arena);
+    sh = dvsg_ctx::Shard{};
+    sh.active = true;
+    sh.nranks = nranks;
+    sh.rank = rank;
+    sh.n_total = n_total;
+    sh.shard_rows = S;
+    sh.gpr_max = 8 * c->num_sms;
+    sh.ring_cap = (uint32_t)pow2_at_least((uint64_t)nranks * sh.gpr_max);
+    sh.arena_bytes = shard_arena_bytes(nranks, sh.gpr_max, sh.ring_cap, c->dpad);
+    cuda_check(cudaMalloc(&sh.arena, sh.arena_bytes), "arena");
+    cuda_check(cudaMemset(sh.arena, 0, sh.arena_bytes), "arena reset");
+  });
+}
+
+dvsg_status dvsg_shard_export(dvsg_ctx* c, void* handle_out) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->sh.active) fail(DVSG_EINVAL, "shard_export: call dvsg_shard_init first");
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, c->sh.arena), "cudaIpcGetMemHandle");
+    std::memcpy(handle_out, &h, sizeof h);
+  });
+}
+
+dvsg_status dvsg_shard_connect(dvsg_ctx* c, const void* handles) {
+  return guarded([&] {
+    set_device(c);
+    auto& sh = c->sh;
+    if (!sh.active) fail(DVSG_EINVAL, "shard_connect: call dvsg_shard_init first");
+    sh.peers.assign((size_t)sh.nranks, nullptr);
+    for (int r = 0; r < sh.nranks; ++r) {
+      if (r == sh.rank) {
+        sh.peers[(size_t)r] = sh.arena;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof h, sizeof h);
+      void* ptr = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      sh.peers[(size_t)r] = static_cast<unsigned char*>(ptr);
+    }
+    sh.connected = true;
+  });
+}
+
+dvsg_status dvsg_shard_prepare(dvsg_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->sh.active) fail(DVSG_EINVAL, "shard_prepare: call dvsg_shard_init first");
+    cuda_check(cudaMemsetAsync(c->sh.arena, 0, c->sh.arena_bytes, c->stream), "arena reset");
+    cuda_check(cudaStreamSynchronize(c->stream), "arena reset");
+  });
+}
+
+dvsg_status dvsg_search_sharded_device(dvsg_ctx* c, const float* d_queries, uint64_t nq, int dim,
+                                       const dvsg_search_params* p, uint32_t* d_out_ids,
+                                       float* d_out_dists, uint32_t* d_out_count, uint64_t* d_out_visited) {
+  return guarded([&] {
+    set_device(c);
+    search_sharded(c, false, c->sh.nranks, d_queries, nq, dim, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
   });
 }
 

@@ -1,0 +1,302 @@
+// k1_device.cuh -- device helpers shared by K1 (search_kernel.cu) and the
+// node-sharded K1 (shard_kernel.cu).  Included inside each .cu translation
+// unit (internal linkage), not a public header.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dvsg_internal.h"
+
+namespace dvsg {
+namespace {
+
+constexpr int kRawPerThread = kChunk / kThreads;  // 8
+
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  if (f == 0.0f) f = 0.0f;  // -0.0 == +0.0 in the reference's comparisons
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  const uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(u);
+}
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t id) { return id * 0x9E3779B1u; }
+
+// Exact insert; returns true when `id` was not present.
+__device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uint32_t id) {
+  uint32_t h = (hash_slot(id) >> 7) & mask;
+  for (;;) {
+    uint32_t cur = table[h];
+    if (cur == id) return false;
+    if (cur == kEmpty) {
+      cur = atomicCAS(table + h, kEmpty, id);
+      if (cur == kEmpty) return true;
+      if (cur == id) return false;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+#ifndef DVSG_SORT_ROLLED
+#define DVSG_SORT_ROLLED 1  // measured: rolled stage loops beat full unroll (I-cache)
+#endif
+#ifndef DVSG_SORT_NOINLINE
+#define DVSG_SORT_NOINLINE 0
+#endif
+#ifndef DVSG_SCORE_ROLLED
+#define DVSG_SCORE_ROLLED 0
+#endif
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a < b ? b : a; }
+
+// Register-tiled bitonic sort of N = KPT * NT keys, ascending.  Element
+// e = t * KPT + r lives in x[r] of thread t.  Partners closer than KPT are in
+// the same thread (register compare-swap), closer than 32 * KPT in the same
+// warp (shuffles); only the remaining stages go through shared memory
+// (r-major, conflict-free) with barriers.  Fully unrolled, but sort_keys is
+// __noinline__ so each kernel carries one copy of each network.
+template <int J, int KPT>
+__device__ __forceinline__ void cmpswap_regs(uint64_t (&x)[KPT], int t, int k) {
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int r2 = r ^ J;
+    if (r2 > r) {
+      const bool up = ((t * KPT + r) & k) == 0;
+      const uint64_t lo = umin64(x[r], x[r2]), hi = umax64(x[r], x[r2]);
+      x[r] = up ? lo : hi;
+      x[r2] = up ? hi : lo;
+    }
+  }
+}
+
+template <int KPT, int NT>
+__device__ __forceinline__ void bitonic_regs(uint64_t (&x)[KPT], int t, uint64_t* s) {
+  constexpr int LOGN = ilog2(KPT * NT);
+#if DVSG_SORT_ROLLED
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+  for (int lk = 1; lk <= LOGN; ++lk) {
+    const int k = 1 << lk;
+#if DVSG_SORT_ROLLED
+#pragma unroll 1
+#else
+#pragma unroll
+#endif
+    for (int lj = lk - 1; lj >= 0; --lj) {
+      const int j = 1 << lj;
+      if (j < KPT) {
+        if (j == 1) cmpswap_regs<1, KPT>(x, t, k);
+        if (KPT > 2 && j == 2) cmpswap_regs<(KPT > 2 ? 2 : 1), KPT>(x, t, k);
+        if (KPT > 4 && j == 4) cmpswap_regs<(KPT > 4 ? 4 : 1), KPT>(x, t, k);
+      } else if (j < KPT * 32) {
+        const int lm = j / KPT;
+        const bool lower = (t & lm) == 0;
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+          const bool up = ((t * KPT + r) & k) == 0;
+          const uint64_t o = __shfl_xor_sync(kFull, x[r], lm);
+          x[r] = (lower == up) ? umin64(x[r], o) : umax64(x[r], o);
+        }
+      } else {
+        const int tm = j / KPT;
+        const bool lower = (t & tm) == 0;
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) s[r * NT + t] = x[r];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < KPT; ++r) {
+          const bool up = ((t * KPT + r) & k) == 0;
+          const uint64_t o = s[r * NT + (t ^ tm)];
+          x[r] = (lower == up) ? umin64(x[r], o) : umax64(x[r], o);
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <int KPT>
+__device__ __forceinline__ void sort_block(uint64_t* s, int n, int tid) {
+  uint64_t x[KPT];
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int e = tid * KPT + r;
+    x[r] = e < n ? s[e] : ~0ull;
+  }
+  __syncthreads();
+  bitonic_regs<KPT, kThreads>(x, tid, s);
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int e = tid * KPT + r;
+    if (e < n) s[e] = x[r];
+  }
+  __syncthreads();
+}
+
+template <int KPT>
+__device__ __forceinline__ void sort_warp0(uint64_t* s, int n, int tid) {
+  if (tid < 32) {
+    uint64_t x[KPT];
+#pragma unroll
+    for (int r = 0; r < KPT; ++r) {
+      const int e = tid * KPT + r;
+      x[r] = e < n ? s[e] : ~0ull;
+    }
+    bitonic_regs<KPT, 32>(x, tid, nullptr);
+#pragma unroll
+    for (int r = 0; r < KPT; ++r) {
+      const int e = tid * KPT + r;
+      if (e < n) s[e] = x[r];
+    }
+  }
+  __syncthreads();
+}
+
+// Plain shared-memory bitonic for the rare n > 2048 (final sort when cap > 2048).
+__device__ void sort_smem_large(uint64_t* s, int n, int tid) {
+  int np = 1;
+  while (np < n) np <<= 1;
+  for (int i = n + tid; i < np; i += kThreads) s[i] = ~0ull;
+  __syncthreads();
+  for (int k = 2; k <= np; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int p = tid; p < (np >> 1); p += kThreads) {
+        const int i = ((p & ~(j - 1)) << 1) | (p & (j - 1));
+        const int ixj = i | j;
+        const uint64_t a = s[i], b = s[ixj];
+        const bool up = (i & k) == 0;
+        if ((a > b) == up) {
+          s[i] = b;
+          s[ixj] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Sort s[0..n) ascending in place (block-uniform call; s holds >= pow2(n)).
+#if DVSG_SORT_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void sort_keys(uint64_t* s, int n, int tid) {
+  if (n <= 1) return;
+  if (n <= 32) return sort_warp0<1>(s, n, tid);
+  if (n <= 64) return sort_warp0<2>(s, n, tid);
+  if (n <= 128) return sort_warp0<4>(s, n, tid);
+  if (n <= 256) return sort_block<1>(s, n, tid);
+  if (n <= 512) return sort_block<2>(s, n, tid);
+  if (n <= 1024) return sort_block<4>(s, n, tid);
+  if (n <= 2048) return sort_block<8>(s, n, tid);
+  return sort_smem_large(s, n, tid);
+}
+
+// out[0..outn) = first outn of merge(A[0..na), B[0..nb)); keys unique.
+// Merge path: each thread owns a contiguous slice of the output.
+__device__ __forceinline__ void merge_path(const uint64_t* A, int na, const uint64_t* B, int nb,
+                                           uint64_t* out, int outn, int tid) {
+  const int per = (outn + kThreads - 1) / kThreads;
+  const int o0 = min(tid * per, outn), o1 = min(o0 + per, outn);
+  if (o0 >= o1) return;
+  int lo = max(0, o0 - nb), hi = min(o0, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (A[mid] < B[o0 - mid - 1]) lo = mid + 1; else hi = mid;
+  }
+  int ia = lo, ib = o0 - lo;
+  for (int o = o0; o < o1; ++o) {
+    const bool takeA = ib >= nb || (ia < na && A[ia] < B[ib]);
+    out[o] = takeA ? A[ia++] : B[ib++];
+  }
+}
+
+// U partial sums per lane -> lane holds the full sum of vector
+// (lane >> (5 - log2 U)) & (U - 1): log2(U) "transpose" stages that halve the
+// live values, then a plain butterfly (U - 1 + 5 - log2 U shuffles instead of 5U).
+template <int U, typename ACC>
+__device__ __forceinline__ ACC transpose_reduce(ACC (&p)[U], int lane) {
+  constexpr int LU = ilog2(U);
+#pragma unroll
+  for (int st = 0; st < LU; ++st) {
+    const int half = U >> (st + 1);
+    const int off = 16 >> st;
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const ACC send = upper ? p[i] : p[i + half];
+      const ACC keep = upper ? p[i + half] : p[i];
+      p[i] = keep + __shfl_xor_sync(kFull, send, off);
+    }
+  }
+  ACC v = p[0];
+#pragma unroll
+  for (int off = 16 >> LU; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  return v;
+}
+
+template <typename ACC, int METRIC>
+__device__ __forceinline__ ACC lane_partial(const float4& x, const float4& q);
+
+template <>
+__device__ __forceinline__ double lane_partial<double, 0>(const float4& x, const float4& q) {
+  // sequential within the lane, no contraction: (x-q)^2 rounded then added
+  const double d0 = (double)x.x - (double)q.x, d1 = (double)x.y - (double)q.y;
+  const double d2 = (double)x.z - (double)q.z, d3 = (double)x.w - (double)q.w;
+  double acc = __dmul_rn(d0, d0);
+  acc = __dadd_rn(acc, __dmul_rn(d1, d1));
+  acc = __dadd_rn(acc, __dmul_rn(d2, d2));
+  acc = __dadd_rn(acc, __dmul_rn(d3, d3));
+  return acc;
+}
+template <>
+__device__ __forceinline__ double lane_partial<double, 1>(const float4& x, const float4& q) {
+  double acc = __dmul_rn((double)x.x, (double)q.x);
+  acc = __dadd_rn(acc, __dmul_rn((double)x.y, (double)q.y));
+  acc = __dadd_rn(acc, __dmul_rn((double)x.z, (double)q.z));
+  acc = __dadd_rn(acc, __dmul_rn((double)x.w, (double)q.w));
+  return acc;
+}
+template <>
+__device__ __forceinline__ float lane_partial<float, 0>(const float4& x, const float4& q) {
+  const float d0 = x.x - q.x, d1 = x.y - q.y, d2 = x.z - q.z, d3 = x.w - q.w;
+  float acc = d0 * d0;
+  acc = fmaf(d1, d1, acc);
+  acc = fmaf(d2, d2, acc);
+  acc = fmaf(d3, d3, acc);
+  return acc;
+}
+template <>
+__device__ __forceinline__ float lane_partial<float, 1>(const float4& x, const float4& q) {
+  float acc = x.x * q.x;
+  acc = fmaf(x.y, q.y, acc);
+  acc = fmaf(x.z, q.z, acc);
+  acc = fmaf(x.w, q.w, acc);
+  return acc;
+}
+
+__device__ __forceinline__ float4 ldg_f4(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+struct BlockState {
+  uint64_t unit;
+  int ncand;
+  int nsurv;
+  int nf;
+  int warp_cnt[kWarps];
+};
+
+}  // namespace
+}  // namespace dvsg

@@ -275,3 +275,35 @@ def test_load_index_format_errors(ctx, tmp_path):
     bad.write_bytes(raw[:-7])
     with pytest.raises(dvs.FormatError, match="truncated"):
         dvs.load_index(str(bad), ctx=ctx)
+
+
+# ---- node-sharded search (ranks emulated in one launch) ------------------------
+
+@pytest.mark.parametrize("nranks", [1, 2, 3, 4, 8])
+def test_sharded_emulated_matches_unsharded(ctx, oracle, nranks):
+    n, dim = 3000, 32
+    v = sift_like(n, dim, 6, 91)
+    adj = oracle.build_graph(v, 32)
+    eo = oracle.compute_entry_order(v)
+    q = sift_like(96, dim, 6, 92)
+    gids = (5 + 2 * np.arange(n)).astype(np.uint32)
+    p = dvs.SearchParams(6, 32, 10, 32, accum="f32")
+    want = oracle.beam_search(v, gids, adj, eo, q, 6, 32, 10, 32)
+    ctx.reset()
+    ctx._single_key = None
+    ctx.load_partition(0, _graph(v, adj, gids, eo))
+    got = ctx.beam_search_sharded_emulated(nranks, q, p)
+    _assert_same(got, want, True, f"sharded R={nranks}")
+
+
+def test_sharded_emulated_golden(ctx, golden):
+    g = golden("g1_uniform.npz")
+    v, adj, q = g["vectors"], g["adjacency"], g["queries"]
+    ctx.reset()
+    ctx._single_key = None
+    ctx.load_partition(0, _graph(v, adj, g["gids"]))
+    for i, (I, w, k, E) in enumerate(g["params"]):
+        p = dvs.SearchParams(int(I), int(w), int(k), int(E), accum="f64")
+        got = ctx.beam_search_sharded_emulated(4, q, p)
+        want = (g[f"ids{i}"], g[f"dists{i}"], g[f"counts{i}"], g[f"visited{i}"])
+        _assert_same(got, want, True, ("sharded golden", i))
