@@ -1,0 +1,27 @@
+"""K1 vs node-sharded K1 with R ranks emulated on one GPU (protocol overhead
+without NVLink): K1 event time for the bench workload, plus parity."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+import paper_2512_02278_b200 as dvs  # noqa: E402
+
+sys.argv = ["x"] + sys.argv[1:]
+args = bench.parse()
+ctx = dvs.Context(0)
+data, queries, index = bench.workload(args, 0, ctx)
+ctx.load_index(index)
+ctx.set_timing(True)
+p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+ref = None
+for _ in range(2):
+    ref = ctx.beam_search(0, queries, p)
+print("unsharded K1 ms", round(ctx.last_timings()["search_ms"], 2), flush=True)
+for R in [1, 2, 4, 8]:
+    for _ in range(2):
+        got = ctx.beam_search_sharded_emulated(R, queries, p)
+    same = all(np.array_equal(a, b) for a, b in zip(got, ref))
+    print(f"emulated R={R} K1 ms", round(ctx.last_timings()["search_ms"], 2), "identical", same, flush=True)
