@@ -266,6 +266,55 @@ def workload_config(args, world, rec):
 
 
 # ---------------------------------------------------------------------------
+def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, index, p, ids_ref,
+                    cnt_ref, flush, dev):
+    """K timed steps of the node-sharded search (vectors split across the N
+    GPUs, fused NVLink frontier exchange); ids must equal the replica run's."""
+    from paper_2512_02278_b200.dist import prepare_step, setup_sharded
+    g0 = index.graphs[0]
+    ctx = dvs.Context(local)
+    setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
+    nq, dim, k = args.nq, args.dim, args.k
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    d_q = torch.from_numpy(queries).to(dev)
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    d_counts = torch.empty((nq,), dtype=torch.int32, device=dev)
+    d_vis = torch.empty((nq,), dtype=torch.int64, device=dev)
+
+    def run():
+        ctx.search_sharded_device(d_q.data_ptr(), nq, dim, p, d_ids.data_ptr(), d_dists.data_ptr(),
+                                  d_counts.data_ptr(), d_vis.data_ptr())
+
+    for _ in range(max(1, args.warmup)):
+        prepare_step(ctx, dist.barrier)
+        run()
+        ctx.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        prepare_step(ctx, dist.barrier)
+        ev0[i].record(stream)
+        run()
+        ev1[i].record(stream)
+        stream.synchronize()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    same = torch.tensor([int(np.array_equal(d_ids.cpu().numpy().view(np.uint32), ids_ref) and
+                             np.array_equal(d_counts.cpu().numpy().view(np.uint32), cnt_ref))],
+                        dtype=torch.int32, device=dev)
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    ctx.close()
+    ms = float(t[0])
+    return {"value": nq * world * args.steps / (ms / 1e3), "unit": "queries/s",
+            "ms_per_step": ms / args.steps,
+            "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; "
+                      "fused NVLink peer-store frontier exchange (shard_kernel.cu)",
+            "ids_identical_to_replica_all_ranks": bool(same[0])}
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -280,12 +329,19 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # rank 0 must print exactly one JSON line on stdout: keep NCCL's version
+        # banner (NCCL_DEBUG=VERSION/INFO) off stdout
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
+            os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     mode = args.mode
     if mode == "auto":
-        mode = "sharded" if world > 1 else "replica"
+        # 1M x 128 (0.64 GB) fits one GPU: replicas are the QPS-optimal layout;
+        # the node-sharded mode is measured beside it at N > 1 (DESIGN.md (e))
+        mode = "replica"
     sharded = mode == "sharded"
     args._sharded = sharded
 
@@ -445,6 +501,12 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": float(e_ms[0]) / args.steps}
 
+    # ---- node-sharded mode beside the replica headline (N > 1) -------------------------
+    sharded_side = None
+    if world > 1 and not sharded and args.mode == "auto":
+        sharded_side = measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries,
+                                       index, p, ids_h, cnt_h, flush, dev)
+
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -494,6 +556,7 @@ def main():
                      "expanded_per_query": exp_tot / max(units_tot, 1)},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "sharded_parity_vs_unsharded": shard_parity,
+        "sharded_mode": sharded_side,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

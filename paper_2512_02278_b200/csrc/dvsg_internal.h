@@ -72,6 +72,7 @@ struct ShardArgs {
   uint32_t mail_stride;
   uint32_t reply_stride;
   uint64_t units_per_rank;       // emulation: rank r owns units [r*upr, (r+1)*upr)
+  int origin_ctas;               // CTAs [0, origin_ctas) of a rank search; the rest only serve
 };
 
 // Comm-arena layout helpers (bytes), shared by host and device.

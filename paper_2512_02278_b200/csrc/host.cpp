@@ -448,6 +448,14 @@ void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uin
   c->d_views.reserve((size_t)nranks, c->stream);
   cuda_check(cudaMemcpyAsync(c->d_views.p, views.data(), views.size() * sizeof(dvsg::ShardView), cudaMemcpyHostToDevice, c->stream), "views");
   sh.views = c->d_views.p;
+  // dedicated server CTAs per rank (drain the doorbell ring promptly)
+  static const int servers_env = [] {
+    const char* e = std::getenv("DVSG_SHARD_SERVERS");
+    return e ? std::atoi(e) : -1;
+  }();
+  int servers = servers_env >= 0 ? servers_env : 0;  // measured: dedicated servers do not pay
+  if (servers >= sh.gpr) servers = sh.gpr - 1;
+  sh.origin_ctas = sh.gpr - servers;
   const int grid_total = emulate ? sh.gpr * nranks : sh.gpr;
   c->hash.reserve((uint64_t)grid_total * k.hsize, c->stream);
   a.hash_global = c->hash.p;

@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kThreads, 4)
   if (uhi > a.nunits) uhi = a.nunits;
   uint32_t myseq = 0;
 
-  for (;;) {
+  // dedicated servers skip the search loop and drain the ring from the start
+  for (; cta < sh.origin_ctas;) {
     if (tid == 0) st.unit = ulo + atomicAdd(mine.work, 1ull);
     __syncthreads();
     const uint64_t unit = st.unit;
@@ -203,6 +204,9 @@ __global__ void __launch_bounds__(kThreads, 4)
 
     const uint32_t qi = a.unit_query[unit];
     const uint32_t n = a.parts[0].n;  // the whole (unsharded) graph
+#ifdef DVSG_SHARD_PROFILE
+    const long long t_unit0 = clock64();
+#endif
 
     float4 q[VPL];
     {
@@ -367,6 +371,10 @@ __global__ void __launch_bounds__(kThreads, 4)
                                     });
         if (expect) {
           // ---- wait for the owners' keys, serving our own ring meanwhile
+#ifdef DVSG_SHARD_PROFILE
+          const long long t_wait0 = clock64();
+          long long t_serve = 0;
+#endif
           for (;;) {
             __syncthreads();
             if (tid == 0) {
@@ -383,12 +391,25 @@ __global__ void __launch_bounds__(kThreads, 4)
             __syncthreads();
             if (ss.ready) break;
             if (ss.job >= 0) {
+#ifdef DVSG_SHARD_PROFILE
+              const long long t0 = clock64();
+#endif
               serve_request<VPL, ACC, METRIC>(sh, me, ss.job, cand, a.dim, a.dpad, lo, tid, lane,
                                               warp);
+#ifdef DVSG_SHARD_PROFILE
+              t_serve += clock64() - t0;
+#endif
             } else if (tid == 0) {
               __nanosleep(64);
             }
           }
+#ifdef DVSG_SHARD_PROFILE
+          if (tid == 0 && a.stats) {
+            atomicAdd(a.stats + 3, (unsigned long long)(clock64() - t_wait0 - t_serve));
+            atomicAdd(a.stats + 4, (unsigned long long)t_serve);
+            atomicAdd(a.stats + 5, 1ull);
+          }
+#endif
           // remote keys through the same exact cap-th-key filter
           for (int d = 0; d < sh.nranks; ++d) {
             if (!(expect >> d & 1u)) continue;
@@ -447,6 +468,9 @@ __global__ void __launch_bounds__(kThreads, 4)
         a.out_dists[unit * (uint64_t)a.k + i] = ord2f((uint32_t)(key >> 32));
       }
     }
+#ifdef DVSG_SHARD_PROFILE
+    if (tid == 0 && a.stats) atomicAdd(a.stats + 6, (unsigned long long)(clock64() - t_unit0));
+#endif
     if (tid == 0) {
       a.out_count[unit] = (uint32_t)want;
       a.out_visited[unit] = visited;
