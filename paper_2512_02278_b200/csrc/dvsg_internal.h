@@ -113,6 +113,8 @@ cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,
 cudaError_t launch_gather_vectors(const uint32_t* ids, const uint32_t* counts, uint64_t nq,
                                   int k, const uint64_t* locator, const float* vectors,
                                   int dim, int dpad, float* out, cudaStream_t stream);
+// Flag bit 2 of *flag when any of x[0..n) is non-finite.
+cudaError_t launch_check_finite(const float* x, uint64_t n, int* flag, cudaStream_t stream);
 // Sum of per-unit visited counters.
 cudaError_t launch_reduce_u64(const uint64_t* in, uint64_t n, unsigned long long* out,
                               cudaStream_t stream);

@@ -161,6 +161,7 @@ struct dvsg_ctx {
   // timing
   bool timing = false;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t mb_ev[2 * 16] = {};  // microbatch pipeline (H2D done, compute done)
   float t_search = 0, t_assign = 0, t_combine = 0, t_total = 0;
   int timing_pending = 0;  // 1: search only, 2: pipeline
   std::atomic<uint64_t> launches{0};
@@ -497,7 +498,7 @@ void build_locator(dvsg_ctx* c) {
 
 void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const dvsg_search_params* p,
                      int fanout, uint32_t* d_ids, float* d_dists, uint32_t* d_count, float* d_vecs,
-                     uint64_t* d_visited) {
+                     uint64_t* d_visited, bool reset_err = true) {
   validate_params(p);
   if (c->clusters < 1) fail(DVSG_EINVAL, "BuiltIndex: index is not built");
   if (dim != c->dim) fail(DVSG_EINVAL, "run_pipeline: query dim %d != index dim %d", dim, c->dim);
@@ -519,7 +520,7 @@ void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const 
     vis = c->u_visited.p;
   }
   c->err_flag.reserve(1, c->stream);
-  cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+  if (reset_err) cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
   c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
   cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->assign_scratch.p, c->stream), "assign");
@@ -650,6 +651,7 @@ dvsg_status dvsg_create(int device, dvsg_ctx** out) {
     cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking), "stream");
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
+    for (auto& e : c->mb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     *out = c.release();
   });
 }
@@ -663,6 +665,7 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
       if ((int)r != c->sh.rank && c->sh.peers[r]) cudaIpcCloseMemHandle(c->sh.peers[r]);
     if (c->sh.arena) cudaFree(c->sh.arena);
     for (auto& e : c->ev) cudaEventDestroy(e);
+    for (auto& e : c->mb_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm);
     delete c;
@@ -1060,28 +1063,64 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
     if (ranks != c->ranks) fail(DVSG_EINVAL, "run_pipeline: placement built for %d ranks, topology has %d", c->ranks, ranks);
     if (nq < 2) fail(DVSG_EINVAL, "run_pipeline: two_microbatch mode needs >= 2 queries");
     if (batch_index < 0) fail(DVSG_EINVAL, "origin_rank_for_batch: negative batch index");
-    if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
     const uint64_t k = (uint64_t)p->k;
-    const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
+    c->io_f.reserve(nq * (uint64_t)dim, c->stream);
     c->io_u.reserve(nq * k + nq, c->stream);
     DevBuf<float>& od = c->io_dists;
     DevBuf<float>& ov = c->io_vecs;
     od.reserve(nq * k, c->stream);
     if (out_vectors) ov.reserve(nq * k * (uint64_t)dim, c->stream);
     c->u_visited.reserve(nq * (uint64_t)fanout, c->stream);
-    if (out_vectors) build_locator(c);
-    pipeline_device(c, d_q, nq, dim, p, fanout, c->io_u.p, od.p, c->io_u.p + nq * k, out_vectors ? ov.p : nullptr, c->u_visited.p);
     c->io_u64.reserve(1, c->stream);
-    cuda_check(dvsg::launch_reduce_u64(c->u_visited.p, nq * (uint64_t)fanout, reinterpret_cast<unsigned long long*>(c->io_u64.p), c->stream), "reduce");
+    c->err_flag.reserve(1, c->stream);
+    if (out_vectors) build_locator(c);
+    sync_slots(c);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+    // Microbatch pipeline -- the reference's two_microbatch schedule
+    // (simulator.cpp:295-297, replay_schedule :111-168) made real: H2D of
+    // batch i+1 and D2H of batch i-1 on the copy stream overlap batch i's
+    // search on the compute stream.  Pinned host buffers are needed for the
+    // copies to be asynchronous.
+    static const uint64_t mb_queries = [] {
+      const char* e = std::getenv("DVSG_MB_QUERIES");
+      return e ? std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) : 25000ull;
+    }();
+    const uint64_t mb = std::max<uint64_t>(2, std::min<uint64_t>(16, nq / mb_queries));
+    cudaEvent_t* evh = c->mb_ev;
+    cudaEvent_t* evc = c->mb_ev + 16;
+    const cudaStream_t cs = c->stream, xs = c->comm;
+    // the copy stream must not start before buffers are reset on the compute stream
+    cuda_check(cudaEventRecord(evc[15], cs), "event");
+    cuda_check(cudaStreamWaitEvent(xs, evc[15], 0), "wait");
+    for (uint64_t i = 0; i < mb; ++i) {
+      const uint64_t q0 = nq * i / mb, q1 = nq * (i + 1) / mb, n_i = q1 - q0;
+      if (n_i == 0) continue;
+      float* dq = c->io_f.p + q0 * (uint64_t)dim;
+      cuda_check(cudaMemcpyAsync(dq, queries + q0 * (uint64_t)dim, n_i * (uint64_t)dim * 4, cudaMemcpyHostToDevice, xs), "H2D");
+      cuda_check(cudaEventRecord(evh[i], xs), "event");
+      cuda_check(cudaStreamWaitEvent(cs, evh[i], 0), "wait");
+      cuda_check(dvsg::launch_check_finite(dq, n_i * (uint64_t)dim, c->err_flag.p, cs), "finite check");
+      c->launches += 1;
+      uint32_t* ids_i = c->io_u.p + q0 * k;
+      uint32_t* cnt_i = c->io_u.p + nq * k + q0;
+      float* d_i = od.p + q0 * k;
+      float* v_i = out_vectors ? ov.p + q0 * k * (uint64_t)dim : nullptr;
+      pipeline_device(c, dq, n_i, dim, p, fanout, ids_i, d_i, cnt_i, v_i, c->u_visited.p + q0 * (uint64_t)fanout, false);
+      cuda_check(cudaEventRecord(evc[i], cs), "event");
+      cuda_check(cudaStreamWaitEvent(xs, evc[i], 0), "wait");
+      cuda_check(cudaMemcpyAsync(out_ids + q0 * k, ids_i, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      cuda_check(cudaMemcpyAsync(out_dists + q0 * k, d_i, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      cuda_check(cudaMemcpyAsync(out_count + q0, cnt_i, n_i * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      if (out_vectors) cuda_check(cudaMemcpyAsync(out_vectors + q0 * k * (uint64_t)dim, v_i, n_i * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+    }
+    cuda_check(dvsg::launch_reduce_u64(c->u_visited.p, nq * (uint64_t)fanout, reinterpret_cast<unsigned long long*>(c->io_u64.p), cs), "reduce");
     c->launches += 1;
     int flag = 0;
-    cuda_check(cudaMemcpyAsync(&flag, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
-    cuda_check(cudaMemcpyAsync(out_ids, c->io_u.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    cuda_check(cudaMemcpyAsync(out_dists, od.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    cuda_check(cudaMemcpyAsync(out_count, c->io_u.p + nq * k, nq * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (out_vectors) cuda_check(cudaMemcpyAsync(out_vectors, ov.p, nq * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    if (visited_total) cuda_check(cudaMemcpyAsync(visited_total, c->io_u64.p, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-    cuda_check(cudaStreamSynchronize(c->stream), "run_pipeline");
+    cuda_check(cudaMemcpyAsync(&flag, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, cs), "D2H");
+    if (visited_total) cuda_check(cudaMemcpyAsync(visited_total, c->io_u64.p, 8, cudaMemcpyDeviceToHost, cs), "D2H");
+    cuda_check(cudaStreamSynchronize(cs), "run_pipeline");
+    cuda_check(cudaStreamSynchronize(xs), "run_pipeline");
+    if (flag & 4) fail(DVSG_EINVAL, "Dataset: non-finite query element");
     if (flag) fail(DVSG_EINTERNAL, "route: cluster id outside placement / not resident, or combine_results: partial list not sorted");
     read_timings(c, true);
   });

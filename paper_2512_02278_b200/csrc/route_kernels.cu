@@ -81,7 +81,7 @@ __global__ void route_kernel(const uint32_t* __restrict__ assign, uint64_t nq, i
   if (u >= nq * (uint64_t)fanout) return;
   const int32_t slot = cluster_to_slot[assign[u]];
   if (slot < 0) {
-    atomicExch(err, 1);
+    atomicOr(err, 1);
     unit_part[u] = 0;
   } else {
     unit_part[u] = (uint32_t)slot;
@@ -109,7 +109,7 @@ __global__ void combine_kernel(uint64_t nq, int nparts, const uint32_t* __restri
     for (uint32_t i = 1; i < cnt; ++i) {
       const uint64_t a = ((uint64_t)f2ord(ld[i - 1]) << 32) | li[i - 1];
       const uint64_t b = ((uint64_t)f2ord(ld[i]) << 32) | li[i];
-      if (b < a) atomicExch(err, 1);  // "partial list not sorted by (dist, id)"
+      if (b < a) atomicOr(err, 1);  // "partial list not sorted by (dist, id)"
     }
   }
   uint32_t* oi = out_ids + q * (uint64_t)k;
@@ -154,6 +154,16 @@ __global__ void gather_vectors_kernel(const uint32_t* __restrict__ ids,
   const float* src = vectors + row * (uint64_t)dpad;
   float* dst = out + slot * (uint64_t)dim;
   for (int i = lane; i < dim; i += 32) dst[i] = src[i];
+}
+
+// Dataset validate (dataset.cpp:18-33) on the device: flag bit 2 if any
+// query element is non-finite, so the host need not scan the batch.
+__global__ void check_finite_kernel(const float* __restrict__ x, uint64_t n, int* flag) {
+  bool bad = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 4);
 }
 
 __global__ void reduce_u64_kernel(const uint64_t* __restrict__ in, uint64_t n,
@@ -210,6 +220,14 @@ cudaError_t launch_gather_vectors(const uint32_t* ids, const uint32_t* counts, u
   const int wpb = 8;
   gather_vectors_kernel<<<(unsigned)((n + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
       ids, counts, nq, k, locator, vectors, dim, dpad, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const float* x, uint64_t n, int* flag, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  uint64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  check_finite_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, n, flag);
   return cudaGetLastError();
 }
 

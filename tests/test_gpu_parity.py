@@ -307,3 +307,27 @@ def test_sharded_emulated_golden(ctx, golden):
         got = ctx.beam_search_sharded_emulated(4, q, p)
         want = (g[f"ids{i}"], g[f"dists{i}"], g[f"counts{i}"], g[f"visited{i}"])
         _assert_same(got, want, True, ("sharded golden", i))
+
+
+def test_pipeline_rejects_non_finite_query(ctx, golden):
+    from fnsy import G3_FNSY
+    res = golden("g3_mixture.npz")
+    dvs.load_index(G3_FNSY, ctx=ctx)
+    q = res["queries"].copy()
+    q[57, 3] = np.nan  # dataset.cpp:18-33
+    with pytest.raises(dvs.InvalidArgument, match="non-finite"):
+        ctx.run_pipeline(q, dvs.SearchParams(6, 16, 10, 16), 2, 4, batch_index=1)
+
+
+def test_pipeline_microbatched_matches_golden(ctx, golden):
+    # 200 golden queries tiled to 60k: several pipelined microbatches, same answers
+    from fnsy import G3_FNSY
+    res = golden("g3_mixture.npz")
+    dvs.load_index(G3_FNSY, ctx=ctx)
+    reps = 300
+    q = np.tile(res["queries"], (reps, 1))
+    r = ctx.run_pipeline(q, dvs.SearchParams(6, 16, 10, 16), 2, 4, batch_index=1)
+    assert np.array_equal(r.counts, np.tile(res["counts_f2"], reps))
+    assert np.array_equal(r.ids, np.tile(res["ids_f2"], (reps, 1)))
+    assert np.array_equal(r.hit_vectors, np.tile(res["vectors_f2"], (reps, 1, 1)))
+    assert r.visited_total == reps * int(res["visited_f2"])
