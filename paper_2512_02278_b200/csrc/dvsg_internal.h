@@ -30,6 +30,7 @@ struct SearchArgs {
   uint64_t nq;
   const uint32_t* unit_query;  // nunits
   const uint32_t* unit_part;   // nunits (partition slot)
+  const uint32_t* unit_order;  // nullable: CTAs claim units in this order (locality); outputs stay per unit
   uint64_t nunits;
   int dim, dpad, dg;
   int iters, beam, k, entry_count, cap;
@@ -113,6 +114,12 @@ cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,
 cudaError_t launch_gather_vectors(const uint32_t* ids, const uint32_t* counts, uint64_t nq,
                                   int k, const uint64_t* locator, const float* vectors,
                                   int dim, int dpad, float* out, cudaStream_t stream);
+// Locality order of units: bucket each unit's query by its nearest anchor
+// (fp32; any order gives identical results), then a counting sort over the
+// buckets.  anchors: na x dpad; scratch: nunits + na + 1 u32.
+cudaError_t launch_locality_order(const float* queries, int dim, const uint32_t* unit_query,
+                                  uint64_t nunits, const float* anchors, int na, int dpad,
+                                  uint32_t* scratch, uint32_t* order, cudaStream_t stream);
 // Flag bit 2 of *flag when any of x[0..n) is non-finite.
 cudaError_t launch_check_finite(const float* x, uint64_t n, int* flag, cudaStream_t stream);
 // Sum of per-unit visited counters.

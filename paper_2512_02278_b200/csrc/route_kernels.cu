@@ -166,6 +166,69 @@ __global__ void check_finite_kernel(const float* __restrict__ x, uint64_t n, int
   if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 4);
 }
 
+// one warp per unit: nearest anchor (fp32, order-only) -> bucket; histogram
+__global__ void anchor_bucket_kernel(const float* __restrict__ queries, int dim,
+                                     const uint32_t* __restrict__ unit_query, uint64_t nunits,
+                                     const float* __restrict__ anchors, int na, int dpad,
+                                     uint32_t* __restrict__ bucket, uint32_t* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t u = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (u >= nunits) return;
+  const float* q = queries + (uint64_t)unit_query[u] * (uint64_t)dim;
+  float qv[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const int i = lane + 32 * v;
+    qv[v] = i < dim ? q[i] : 0.f;
+  }
+  float best = 3.4e38f;
+  int besti = 0;
+  for (int a = 0; a < na; ++a) {
+    const float* av = anchors + (uint64_t)a * dpad;
+    float acc = 0.f;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int i = lane + 32 * v;
+      if (i < dim) {
+        const float d = qv[v] - av[i];
+        acc = fmaf(d, d, acc);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (acc < best) {
+      best = acc;
+      besti = a;
+    }
+  }
+  if (lane == 0) {
+    bucket[u] = (uint32_t)besti;
+    atomicAdd(hist + besti, 1u);
+  }
+}
+
+__global__ void exclusive_scan_small(uint32_t* __restrict__ hist, int n) {
+  // single block; n <= 1024
+  __shared__ uint32_t s[1024];
+  const int t = threadIdx.x;
+  s[t] = t < n ? hist[t] : 0u;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const uint32_t v = t >= off ? s[t - off] : 0u;
+    __syncthreads();
+    s[t] += v;
+    __syncthreads();
+  }
+  if (t < n) hist[t] = t == 0 ? 0u : s[t - 1];
+}
+
+__global__ void bucket_scatter_kernel(const uint32_t* __restrict__ bucket, uint64_t nunits,
+                                      uint32_t* __restrict__ offs, uint32_t* __restrict__ order) {
+  const uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nunits) return;
+  order[atomicAdd(offs + bucket[u], 1u)] = (uint32_t)u;
+}
+
 __global__ void reduce_u64_kernel(const uint64_t* __restrict__ in, uint64_t n,
                                   unsigned long long* out) {
   unsigned long long acc = 0;
@@ -228,6 +291,24 @@ cudaError_t launch_check_finite(const float* x, uint64_t n, int* flag, cudaStrea
   uint64_t blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
   check_finite_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_locality_order(const float* queries, int dim, const uint32_t* unit_query,
+                                  uint64_t nunits, const float* anchors, int na, int dpad,
+                                  uint32_t* scratch, uint32_t* order, cudaStream_t stream) {
+  if (nunits == 0) return cudaSuccess;
+  if (na < 1 || na > 1024 || dim > 256) return cudaErrorInvalidValue;
+  uint32_t* bucket = scratch;
+  uint32_t* hist = scratch + nunits;
+  cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)na, stream);
+  if (e != cudaSuccess) return e;
+  const int wpb = 8;
+  anchor_bucket_kernel<<<(unsigned)((nunits + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
+      queries, dim, unit_query, nunits, anchors, na, dpad, bucket, hist);
+  exclusive_scan_small<<<1, 1024, 0, stream>>>(hist, na);
+  bucket_scatter_kernel<<<(unsigned)((nunits + 255) / 256), 256, 0, stream>>>(bucket, nunits, hist,
+                                                                             order);
   return cudaGetLastError();
 }
 

@@ -57,7 +57,10 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   const unsigned lt_mask = (1u << lane) - 1u;
 
   for (;;) {
-    if (tid == 0) st.unit = atomicAdd(a.work_counter, 1ull);
+    if (tid == 0) {
+      const unsigned long long ticket = atomicAdd(a.work_counter, 1ull);
+      st.unit = (a.unit_order && ticket < a.nunits) ? a.unit_order[ticket] : ticket;
+    }
     __syncthreads();
     const uint64_t unit = st.unit;
     if (unit >= a.nunits) return;

@@ -331,3 +331,41 @@ def test_pipeline_microbatched_matches_golden(ctx, golden):
     assert np.array_equal(r.ids, np.tile(res["ids_f2"], (reps, 1)))
     assert np.array_equal(r.hit_vectors, np.tile(res["vectors_f2"], (reps, 1, 1)))
     assert r.visited_total == reps * int(res["visited_f2"])
+
+
+# ---- BASELINE config shapes at parity-test scale (configs[2..4]) ---------------
+
+def test_cfg4_shape_ip768_k100_beam256(ctx, oracle):
+    # text-embedding-like: 768-d, L2-normalised, inner product, top-100, beam 256
+    # (pool cap 3072 > 2048 -> the large final-sort path; visited bound > 16k)
+    n, dim = 4000, 768
+    rng = np.random.default_rng(4)
+    basis = rng.normal(size=(32, dim)).astype(np.float32)
+    v = (rng.normal(size=(n, 32)).astype(np.float32) @ basis)
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    q = (rng.normal(size=(24, 32)).astype(np.float32) @ basis)
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    adj = oracle.build_graph(v, 32)
+    eo = oracle.compute_entry_order(v)
+    gids = np.arange(n, dtype=np.uint32)
+    want = oracle.beam_search(v, gids, adj, eo, q, 6, 256, 100, 256, metric=1)
+    got = _search(ctx, v, adj, q, dvs.SearchParams(6, 256, 100, 256, metric="ip", accum="f64"))
+    _assert_same(got, want, True, "cfg4-shape f64")
+    got32 = _search(ctx, v, adj, q, dvs.SearchParams(6, 256, 100, 256, metric="ip", accum="f32"))
+    same = sum(np.array_equal(got32[0][j, :got32[2][j]], want[0][j, :want[2][j]]) for j in range(len(q)))
+    assert same >= 0.9 * len(q)
+    np.testing.assert_allclose(got32[1][:, :10], want[1][:, :10], rtol=1e-4, atol=1e-5)
+
+
+def test_cfg3_shape_d96_beam_sweep(ctx, oracle):
+    # Deep-like 96-d, top-10, the cfg5 beam sweep 32..256
+    n, dim = 6000, 96
+    v = oracle.random_dataset(n, dim, 96)
+    adj = oracle.build_graph(v, 32)
+    eo = oracle.compute_entry_order(v)
+    q = oracle.random_dataset(32, dim, 97)
+    gids = np.arange(n, dtype=np.uint32)
+    for w in (32, 64, 128, 256):
+        want = oracle.beam_search(v, gids, adj, eo, q, 6, w, 10, w)
+        got = _search(ctx, v, adj, q, dvs.SearchParams(6, w, 10, w, accum="f64"))
+        _assert_same(got, want, True, f"cfg3-shape w={w}")
