@@ -366,8 +366,14 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   }
   int max_grid = 0;
   if (!k.hash_in_smem) {
-    // one L2-resident region per persistent CTA
+    // one L2-resident region per persistent CTA; optionally cap the grid so
+    // the tables' total footprint stays within an L2 budget (large beams)
     max_grid = 8 * c->num_sms;
+    static const uint64_t l2_budget = [] {
+      const char* e = std::getenv("DVSG_HASH_L2_BUDGET_MB");
+      return e ? std::strtoull(e, nullptr, 10) << 20 : 0ull;
+    }();
+    if (l2_budget) max_grid = (int)std::max<uint64_t>((uint64_t)c->num_sms, std::min<uint64_t>((uint64_t)max_grid, l2_budget / (4 * k.hsize)));
     c->hash.reserve((uint64_t)max_grid * k.hsize, c->stream);
     a.hash_global = c->hash.p;
   }

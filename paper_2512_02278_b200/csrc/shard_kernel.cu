@@ -37,6 +37,10 @@
 namespace dvsg {
 namespace {
 
+#ifndef DVSG_SHARD_FENCE_ALL
+#define DVSG_SHARD_FENCE_ALL 0  // 1: every storing thread fences (conservative)
+#endif
+
 static_assert(kChunk == 2048, "shard_mail_stride/shard_reply_stride assume kChunk == 2048");
 
 __device__ __forceinline__ uint32_t ld_cg_u32(const void* p) {
@@ -146,9 +150,12 @@ __device__ void serve_request(const ShardArgs& sh, int me, int job, uint32_t* ca
                               [&](bool valid, int ci, uint64_t key) {
                                 if (valid) keys[ci] = key;  // NVLink peer store
                               });
+#if DVSG_SHARD_FENCE_ALL
   __threadfence_system();
+#endif
   __syncthreads();
   if (tid == 0) {
+    __threadfence_system();  // release the whole CTA's key stores (cumulative after the barrier)
     volatile uint32_t* hdr = reinterpret_cast<volatile uint32_t*>(rb);
     hdr[1] = (uint32_t)cnt;
     __threadfence_system();
@@ -349,9 +356,14 @@ __global__ void __launch_bounds__(kThreads, 4)
             }
             pushed = true;
           }
+#if DVSG_SHARD_FENCE_ALL
           if (pushed) __threadfence_system();  // release this thread's peer stores
+#endif
           __syncthreads();
           if (tid < sh.nranks && (expect >> tid & 1u)) {
+            // release (cumulative fence after the CTA barrier, as in grid sync):
+            // every thread's mailbox stores are ordered before the doorbell
+            __threadfence_system();
             const ShardView& dst = sh.views[tid];
             const unsigned slot = atomicAdd(dst.ring_tail, 1u);
             reinterpret_cast<volatile uint32_t*>(dst.ring)[slot & sh.ring_mask] =
