@@ -332,7 +332,7 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   if (c->parts.empty()) fail(DVSG_EINVAL, "beam_search: empty graph");
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (nunits == 0) return;
-  if ((uint64_t)p->beam_width * (uint64_t)c->dg > (1ull << 30)) fail(DVSG_EINVAL, "beam_search: beam_width * out_degree too large");
+  if ((uint64_t)p->beam_width * (uint64_t)c->dg > (1ull << 24)) fail(DVSG_EINVAL, "beam_search: beam_width * out_degree above 2^24 candidates per iteration");
   sync_parts(c);
   uint64_t nmax = 0;
   for (auto& pd : c->parts) nmax = std::max<uint64_t>(nmax, pd.n);

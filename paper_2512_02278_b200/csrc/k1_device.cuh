@@ -63,16 +63,21 @@ __device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a < 
 // warp (shuffles); only the remaining stages go through shared memory
 // (r-major, conflict-free) with barriers.  Fully unrolled, but sort_keys is
 // __noinline__ so each kernel carries one copy of each network.
+// Element e = t*KPT + r with t*KPT a multiple of KPT, so the direction bit
+// (e & k) is (r & k) for k < KPT (a compile-time constant per register) and
+// (t*KPT & k) for k >= KPT (one bit per stage, shared by all r).
 template <int J, int KPT>
-__device__ __forceinline__ void cmpswap_regs(uint64_t (&x)[KPT], int t, int k) {
+__device__ __forceinline__ void cmpswap_regs(uint64_t (&x)[KPT], int e0, int k) {
+  const bool up_hi = (e0 & k) == 0;
 #pragma unroll
   for (int r = 0; r < KPT; ++r) {
     const int r2 = r ^ J;
     if (r2 > r) {
-      const bool up = ((t * KPT + r) & k) == 0;
-      const uint64_t lo = umin64(x[r], x[r2]), hi = umax64(x[r], x[r2]);
-      x[r] = up ? lo : hi;
-      x[r2] = up ? hi : lo;
+      const bool up = k < KPT ? ((r & k) == 0) : up_hi;
+      const uint64_t a = x[r], b = x[r2];
+      const bool sw = (b < a) == up;  // keys unique: never equal
+      x[r] = sw ? b : a;
+      x[r2] = sw ? a : b;
     }
   }
 }
@@ -80,6 +85,7 @@ __device__ __forceinline__ void cmpswap_regs(uint64_t (&x)[KPT], int t, int k) {
 template <int KPT, int NT>
 __device__ __forceinline__ void bitonic_regs(uint64_t (&x)[KPT], int t, uint64_t* s) {
   constexpr int LOGN = ilog2(KPT * NT);
+  const int e0 = t * KPT;
 #if DVSG_SORT_ROLLED
 #pragma unroll 1
 #else
@@ -87,6 +93,7 @@ __device__ __forceinline__ void bitonic_regs(uint64_t (&x)[KPT], int t, uint64_t
 #endif
   for (int lk = 1; lk <= LOGN; ++lk) {
     const int k = 1 << lk;
+    const bool up_stage = (e0 & k) == 0;  // valid for every stage with k >= KPT
 #if DVSG_SORT_ROLLED
 #pragma unroll 1
 #else
@@ -95,29 +102,27 @@ __device__ __forceinline__ void bitonic_regs(uint64_t (&x)[KPT], int t, uint64_t
     for (int lj = lk - 1; lj >= 0; --lj) {
       const int j = 1 << lj;
       if (j < KPT) {
-        if (j == 1) cmpswap_regs<1, KPT>(x, t, k);
-        if (KPT > 2 && j == 2) cmpswap_regs<(KPT > 2 ? 2 : 1), KPT>(x, t, k);
-        if (KPT > 4 && j == 4) cmpswap_regs<(KPT > 4 ? 4 : 1), KPT>(x, t, k);
+        if (j == 1) cmpswap_regs<1, KPT>(x, e0, k);
+        if (KPT > 2 && j == 2) cmpswap_regs<(KPT > 2 ? 2 : 1), KPT>(x, e0, k);
+        if (KPT > 4 && j == 4) cmpswap_regs<(KPT > 4 ? 4 : 1), KPT>(x, e0, k);
       } else if (j < KPT * 32) {
         const int lm = j / KPT;
-        const bool lower = (t & lm) == 0;
+        const bool keep_min = ((t & lm) == 0) == up_stage;
 #pragma unroll
         for (int r = 0; r < KPT; ++r) {
-          const bool up = ((t * KPT + r) & k) == 0;
           const uint64_t o = __shfl_xor_sync(kFull, x[r], lm);
-          x[r] = (lower == up) ? umin64(x[r], o) : umax64(x[r], o);
+          x[r] = ((o < x[r]) == keep_min) ? o : x[r];
         }
       } else {
         const int tm = j / KPT;
-        const bool lower = (t & tm) == 0;
+        const bool keep_min = ((t & tm) == 0) == up_stage;
 #pragma unroll
         for (int r = 0; r < KPT; ++r) s[r * NT + t] = x[r];
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < KPT; ++r) {
-          const bool up = ((t * KPT + r) & k) == 0;
           const uint64_t o = s[r * NT + (t ^ tm)];
-          x[r] = (lower == up) ? umin64(x[r], o) : umax64(x[r], o);
+          x[r] = ((o < x[r]) == keep_min) ? o : x[r];
         }
         __syncthreads();
       }

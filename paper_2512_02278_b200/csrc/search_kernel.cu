@@ -35,7 +35,8 @@ namespace dvsg {
 namespace {
 
 // VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
-template <int VPL, typename ACC, int METRIC>
+// FULL: dpad == 128 * VPL (every lane holds real dimensions; no bound check).
+template <int VPL, typename ACC, int METRIC, bool FULL>
 #ifndef DVSG_MINB
 #define DVSG_MINB 5  // resident CTAs per SM the register budget is cut for (measured sweep)
 #endif
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   uint32_t* table = a.hash_global ? a.hash_global + (size_t)blockIdx.x * (size_t)a.hsize
                                   : frontier + ((a.beam + 3) & ~3);
   const uint32_t hmask = (uint32_t)a.hsize - 1u;
+  const uint32_t dg_magic = (uint32_t)((0x100000000ull + (uint64_t)a.dg - 1) / (uint64_t)a.dg);
   const unsigned full = 0xFFFFFFFFu;
   const unsigned lt_mask = (1u << lane) - 1u;
 
@@ -70,6 +72,9 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
     const uint64_t row0 = part.row_off;
     const uint32_t n = part.n;
     const float* vbase = a.vectors + row0 * (uint64_t)a.dpad;
+    const float* lbase = vbase + lane * 4;          // this lane's first dims of row 0
+    const uint32_t* abase = a.adjacency + row0 * (uint64_t)a.dg;
+    const uint32_t rstride = (uint32_t)a.dpad;      // u32 x u32 -> u64: one IMAD.WIDE per row
 
     // query slice in registers: lane holds dims [lane*4 + 128 v, +4)
     float4 q[VPL];
@@ -151,8 +156,13 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
             if (it < 0) {
               ids[j] = __ldg(a.entry + row0 + g);
             } else {
-              const int f = g / a.dg, jj = g - f * a.dg;
-              ids[j] = __ldg(a.adjacency + (row0 + frontier[f]) * (uint64_t)a.dg + jj);
+              // g / dg by multiply-high with m = ceil(2^32/dg): exact while
+              // g * (m*dg - 2^32) < 2^32, i.e. g < 2^24 and dg < 256 (host-checked);
+              // dg == 1 overflows m, dg >= 256 takes the plain division
+              const uint32_t f = a.dg == 1 ? (uint32_t)g
+                               : (a.dg < 256 ? __umulhi((uint32_t)g, dg_magic) : (uint32_t)g / (uint32_t)a.dg);
+              const uint32_t jj = (uint32_t)g - f * (uint32_t)a.dg;
+              ids[j] = __ldg(abase + (uint64_t)frontier[f] * (uint32_t)a.dg + jj);
             }
           }
         }
@@ -190,12 +200,12 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           float4 x[U][VPL];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            const bool valid = cb + u < M;
-            const float* row = vbase + (uint64_t)ids_u[u] * (uint64_t)a.dpad;
+            // past M: load row 0 (harmless, result discarded by the ci < M test)
+            const uint32_t id = cb + u < M ? ids_u[u] : 0u;
+            const float* row = lbase + (uint64_t)id * rstride;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
-              const int b = lane * 4 + 128 * v;
-              if (valid && b < a.dpad) x[u][v] = ldg_f4(row + b);
+              if (FULL || lane * 4 + 128 * v < a.dpad) x[u][v] = ldg_f4(row + 128 * v);
               else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
@@ -290,10 +300,10 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   }
 }
 
-template <int VPL, typename ACC, int METRIC>
+template <int VPL, typename ACC, int METRIC, bool FULL>
 cudaError_t launch_t(const SearchArgs& a, int num_sms, int max_grid, cudaStream_t stream,
                      int* grid_out) {
-  auto kern = search_kernel<VPL, ACC, METRIC>;
+  auto kern = search_kernel<VPL, ACC, METRIC, FULL>;
   const size_t smem = search_smem_bytes(a.cap, a.chp, a.beam, a.hsize, a.hash_global == nullptr);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -313,12 +323,17 @@ cudaError_t launch_t(const SearchArgs& a, int num_sms, int max_grid, cudaStream_
 template <int VPL>
 cudaError_t launch_v(const SearchArgs& a, int metric, int accum, int num_sms, int mg,
                      cudaStream_t s, int* g) {
+  const bool full = a.dpad == 128 * VPL;
   if (accum == 0) {
-    return metric == 0 ? launch_t<VPL, double, 0>(a, num_sms, mg, s, g)
-                       : launch_t<VPL, double, 1>(a, num_sms, mg, s, g);
+    if (metric == 0) return full ? launch_t<VPL, double, 0, true>(a, num_sms, mg, s, g)
+                                 : launch_t<VPL, double, 0, false>(a, num_sms, mg, s, g);
+    return full ? launch_t<VPL, double, 1, true>(a, num_sms, mg, s, g)
+                : launch_t<VPL, double, 1, false>(a, num_sms, mg, s, g);
   }
-  return metric == 0 ? launch_t<VPL, float, 0>(a, num_sms, mg, s, g)
-                     : launch_t<VPL, float, 1>(a, num_sms, mg, s, g);
+  if (metric == 0) return full ? launch_t<VPL, float, 0, true>(a, num_sms, mg, s, g)
+                               : launch_t<VPL, float, 0, false>(a, num_sms, mg, s, g);
+  return full ? launch_t<VPL, float, 1, true>(a, num_sms, mg, s, g)
+              : launch_t<VPL, float, 1, false>(a, num_sms, mg, s, g);
 }
 
 }  // namespace

@@ -21,6 +21,7 @@ for I, w in [(6, 64)]:
     c = np.zeros(16, np.uint64)
     lib.dvsg_debug_counters(ctx.handle, ctypes.c_void_p(c.ctypes.data))
     nq = queries.shape[0]
-    print(dict(units=int(c[1]), visited_per_q=c[2] / nq, expanded_per_q=c[3] / nq,
-               S_per_q=c[4] / nq, Sp_per_q=c[5] / nq, chunks_per_q=c[6] / nq,
-               S_entry=c[7] / nq, S_iter0=c[8] / nq, S_later=c[9] / nq, M_per_q=c[10] / nq))
+    print(dict(units=int(c[1]), visited_per_q=round(c[2] / nq, 1), expanded_per_q=round(c[3] / nq, 1),
+               survivors_sorted_per_q=round(c[4] / nq, 1), new_local_per_q=round(c[5] / nq, 1),
+               chunks_per_q=round(c[6] / nq, 2), S_entry=round(c[7] / nq, 1),
+               S_first_expansion=round(c[8] / nq, 1), S_later_total=round(c[9] / nq, 1)))

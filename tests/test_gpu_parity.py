@@ -369,3 +369,17 @@ def test_cfg3_shape_d96_beam_sweep(ctx, oracle):
         want = oracle.beam_search(v, gids, adj, eo, q, 6, w, 10, w)
         got = _search(ctx, v, adj, q, dvs.SearchParams(6, w, 10, w, accum="f64"))
         _assert_same(got, want, True, f"cfg3-shape w={w}")
+
+
+@pytest.mark.parametrize("dg", [1, 2, 3, 33])
+def test_odd_degrees_match_oracle(ctx, oracle, dg):
+    # exercises the multiply-high row index (dg == 1 special case, non-pow2 degrees)
+    n, dim = 700, 16
+    v = oracle.random_dataset(n, dim, 300 + dg)
+    adj = oracle.build_graph(v, dg)
+    eo = oracle.compute_entry_order(v)
+    q = oracle.random_dataset(40, dim, 400 + dg)
+    gids = np.arange(n, dtype=np.uint32)
+    want = oracle.beam_search(v, gids, adj, eo, q, 8, 24, 10, 8)
+    got = _search(ctx, v, adj, q, dvs.SearchParams(8, 24, 10, 8, accum="f64"))
+    _assert_same(got, want, True, f"dg={dg}")
