@@ -26,9 +26,17 @@ __device__ __forceinline__ float ord2f(uint32_t o) {
 __device__ __forceinline__ uint32_t hash_slot(uint32_t id) { return id * 0x9E3779B1u; }
 
 // Exact insert; returns true when `id` was not present.
+#ifndef DVSG_HASH_CAS_FIRST
+#define DVSG_HASH_CAS_FIRST 0  // measured: CAS-first -10% (the plain probe loads hit L1)
+#endif
 __device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uint32_t id) {
   uint32_t h = (hash_slot(id) >> 7) & mask;
   for (;;) {
+#if DVSG_HASH_CAS_FIRST
+    const uint32_t cur = atomicCAS(table + h, kEmpty, id);  // claims the slot or returns its id
+    if (cur == kEmpty) return true;
+    if (cur == id) return false;
+#else
     uint32_t cur = table[h];
     if (cur == id) return false;
     if (cur == kEmpty) {
@@ -36,6 +44,7 @@ __device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uin
       if (cur == kEmpty) return true;
       if (cur == id) return false;
     }
+#endif
     h = (h + 1) & mask;
   }
 }
@@ -291,8 +300,30 @@ __device__ __forceinline__ float lane_partial<float, 1>(const float4& x, const f
   return acc;
 }
 
+#ifndef DVSG_GATHER_NO_L1
+#define DVSG_GATHER_NO_L1 2  // 1: vector rows bypass L1 (+5%), 2: adjacency rows too (+1%)
+#endif
+// Vector rows are streamed (little L1 reuse): optionally keep them out of L1
+// so the CTA's visited-table lines stay cached there.
 __device__ __forceinline__ float4 ldg_f4(const float* p) {
+#if DVSG_GATHER_NO_L1
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+#else
   return __ldg(reinterpret_cast<const float4*>(p));
+#endif
+}
+
+__device__ __forceinline__ uint32_t ldg_u32_stream(const uint32_t* p) {
+#if DVSG_GATHER_NO_L1 >= 2
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+#else
+  return __ldg(p);
+#endif
 }
 
 struct BlockState {

@@ -41,7 +41,10 @@ template <int VPL, typename ACC, int METRIC, bool FULL>
 #define DVSG_MINB 5  // resident CTAs per SM the register budget is cut for (measured sweep)
 #endif
 __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const SearchArgs a) {
-  constexpr int U = VPL >= 8 ? 1 : (8 / VPL);
+#ifndef DVSG_UVEC
+#define DVSG_UVEC 8  // vectors in flight per warp at VPL == 1 (measured sweep)
+#endif
+  constexpr int U = VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL);
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ BlockState st;
 
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
               const uint32_t f = a.dg == 1 ? (uint32_t)g
                                : (a.dg < 256 ? __umulhi((uint32_t)g, dg_magic) : (uint32_t)g / (uint32_t)a.dg);
               const uint32_t jj = (uint32_t)g - f * (uint32_t)a.dg;
-              ids[j] = __ldg(abase + (uint64_t)frontier[f] * (uint32_t)a.dg + jj);
+              ids[j] = ldg_u32_stream(abase + (uint64_t)frontier[f] * (uint32_t)a.dg + jj);
             }
           }
         }
