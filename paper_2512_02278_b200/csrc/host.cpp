@@ -1129,12 +1129,30 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
     // the copy stream must not start before buffers are reset on the compute stream
     cuda_check(cudaEventRecord(evc[15], cs), "event");
     cuda_check(cudaStreamWaitEvent(xs, evc[15], 0), "wait");
+    // decreasing microbatch sizes (weights mb, mb-1, ..., 1): the last D2H --
+    // the only copy nothing overlaps -- is the smallest
+    static const bool taper = [] {
+      const char* e = std::getenv("DVSG_MB_TAPER");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    const uint64_t wsum = taper ? mb * (mb + 1) / 2 : mb;
+    auto edge = [&](uint64_t i) -> uint64_t {  // prefix of the first i microbatches
+      const uint64_t w = taper ? i * mb - i * (i - 1) / 2 : i;
+      return nq * w / wsum;
+    };
+    // every H2D first: a D2H queued on the copy stream waits for its batch's
+    // compute, so an H2D queued behind it would serialize the whole pipeline
     for (uint64_t i = 0; i < mb; ++i) {
-      const uint64_t q0 = nq * i / mb, q1 = nq * (i + 1) / mb, n_i = q1 - q0;
+      const uint64_t q0 = edge(i), n_i = edge(i + 1) - q0;
+      if (n_i == 0) continue;
+      cuda_check(cudaMemcpyAsync(c->io_f.p + q0 * (uint64_t)dim, queries + q0 * (uint64_t)dim,
+                                 n_i * (uint64_t)dim * 4, cudaMemcpyHostToDevice, xs), "H2D");
+      cuda_check(cudaEventRecord(evh[i], xs), "event");
+    }
+    for (uint64_t i = 0; i < mb; ++i) {
+      const uint64_t q0 = edge(i), q1 = edge(i + 1), n_i = q1 - q0;
       if (n_i == 0) continue;
       float* dq = c->io_f.p + q0 * (uint64_t)dim;
-      cuda_check(cudaMemcpyAsync(dq, queries + q0 * (uint64_t)dim, n_i * (uint64_t)dim * 4, cudaMemcpyHostToDevice, xs), "H2D");
-      cuda_check(cudaEventRecord(evh[i], xs), "event");
       cuda_check(cudaStreamWaitEvent(cs, evh[i], 0), "wait");
       cuda_check(dvsg::launch_check_finite(dq, n_i * (uint64_t)dim, c->err_flag.p, cs), "finite check");
       c->launches += 1;
