@@ -199,6 +199,14 @@ dvsg_status dvsg_run_pipeline_device(dvsg_ctx *ctx, const float *d_queries, uint
 dvsg_status dvsg_build_graph(dvsg_ctx *ctx, const float *vectors, uint64_t n, int dim,
                              int out_degree, uint32_t *adjacency_out);
 
+/* ---- ground truth (brute_force_topk, topk.cpp:12-30) ---------------------
+ * Exact top-k by (dist, id) of nq queries over the n x dim database (host
+ * buffers), k <= 32; fp32 distances over (x - y)^2, exact for integer-valued
+ * data.  Used for recall@k at sizes the CPU oracle cannot reach. */
+dvsg_status dvsg_brute_force_topk(dvsg_ctx *ctx, const float *db, uint64_t n, int dim,
+                                  const float *queries, uint64_t nq, int k, uint32_t *out_ids,
+                                  float *out_dists);
+
 /* ---- instrumentation ---------------------------------------------------- */
 /* Device time (ms) of the last search kernel launch (K1) and of the whole
  * last pipeline call, measured with CUDA events on the compute stream;

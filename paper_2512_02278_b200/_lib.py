@@ -75,6 +75,8 @@ _SIGS = {
     "dvsg_run_pipeline_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, P_params, c_int,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dvsg_build_graph": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
+    "dvsg_brute_force_topk": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_uint64, c_int,
+                                      c_void_p, c_void_p]),
     "dvsg_set_timing": (c_int, [c_void_p, c_int]),
     "dvsg_last_timings": (c_int, [c_void_p, P_f32, P_f32, P_f32, P_f32]),
     "dvsg_kernel_launches": (c_uint64, [c_void_p]),

@@ -367,6 +367,18 @@ class Context:
                                            ctypes.c_void_p(d_vectors or None),
                                            ctypes.c_void_p(d_visited or None)))
 
+    def brute_force_topk(self, db, queries, k: int):
+        """topk.cpp:12-30 on the GPU -> (ids nq x k, dists nq x k)."""
+        d = _f32(db, 2)
+        q = _f32(queries, 2)
+        if q.shape[1] != d.shape[1]:
+            raise InvalidArgument("brute_force_topk: dimension mismatch")
+        ids = np.zeros((q.shape[0], max(int(k), 1)), np.uint32)
+        dists = np.zeros((q.shape[0], max(int(k), 1)), np.float32)
+        check(lib.dvsg_brute_force_topk(self._h, _ptr(d), d.shape[0], d.shape[1], _ptr(q), q.shape[0],
+                                        int(k), _ptr(ids), _ptr(dists)))
+        return ids, dists
+
     # ---- timing --------------------------------------------------------------
     def set_timing(self, on: bool) -> None:
         check(lib.dvsg_set_timing(self._h, 1 if on else 0))

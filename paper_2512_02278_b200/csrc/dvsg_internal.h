@@ -126,6 +126,10 @@ cudaError_t launch_check_finite(const float* x, uint64_t n, int* flag, cudaStrea
 cudaError_t launch_reduce_u64(const uint64_t* in, uint64_t n, unsigned long long* out,
                               cudaStream_t stream);
 
+// Exact brute-force top-k (topk.cpp:12-30) of nq queries over n rows (k <= 32).
+cudaError_t launch_brute_force(const float* queries, uint64_t nq, const float* db, uint64_t n,
+                               int dpad, int k, uint32_t* out_ids, float* out_dists,
+                               cudaStream_t stream);
 // K6 exact kNN graph rows (knn_build.cu)
 cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad,
                              int out_degree, uint32_t* adjacency, cudaStream_t stream);

@@ -1215,6 +1215,35 @@ dvsg_status dvsg_build_graph(dvsg_ctx* c, const float* vectors, uint64_t n, int 
   });
 }
 
+dvsg_status dvsg_brute_force_topk(dvsg_ctx* c, const float* db, uint64_t n, int dim, const float* queries,
+                                  uint64_t nq, int k, uint32_t* out_ids, float* out_dists) {
+  return guarded([&] {
+    set_device(c);
+    if (n == 0) fail(DVSG_EINVAL, "brute_force_topk: empty database");
+    if (k < 1 || (uint64_t)k > n) fail(DVSG_EINVAL, "brute_force_topk: k=%d out of range for database of size %llu", k, (unsigned long long)n);
+    if (k > 32) fail(DVSG_EINVAL, "brute_force_topk: k=%d above the device limit 32", k);
+    if (dim < 1) fail(DVSG_EINVAL, "Dataset: dim must be positive, got %d", dim);
+    if (nq == 0) return;
+    const int dpad = (dim + 3) & ~3;
+    DevBuf<float> dd, dq;
+    DevBuf<uint32_t> oi;
+    DevBuf<float> od;
+    dd.reserve(n * (uint64_t)dpad, c->stream);
+    dq.reserve(nq * (uint64_t)dpad, c->stream);
+    oi.reserve(nq * (uint64_t)k, c->stream);
+    od.reserve(nq * (uint64_t)k, c->stream);
+    cuda_check(cudaMemset(dd.p, 0, n * (uint64_t)dpad * 4), "memset");
+    cuda_check(cudaMemset(dq.p, 0, nq * (uint64_t)dpad * 4), "memset");
+    cuda_check(cudaMemcpy2D(dd.p, (size_t)dpad * 4, db, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy2D(dq.p, (size_t)dpad * 4, queries, (size_t)dim * 4, (size_t)dim * 4, nq, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(dvsg::launch_brute_force(dq.p, nq, dd.p, n, dpad, k, oi.p, od.p, c->stream), "brute force");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "brute force");
+    cuda_check(cudaMemcpy(out_ids, oi.p, nq * (uint64_t)k * 4, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(out_dists, od.p, nq * (uint64_t)k * 4, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
 dvsg_status dvsg_set_timing(dvsg_ctx* c, int enabled) {
   return guarded([&] { c->timing = enabled != 0; });
 }

@@ -33,9 +33,14 @@ __device__ __forceinline__ uint32_t f2ord(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__global__ void __launch_bounds__(256) knn_kernel(const float* __restrict__ vec, uint64_t n,
-                                                  int dpad, int deg,
-                                                  uint32_t* __restrict__ adj) {
+// rows x cols exact top-`deg` by (dist, id).  Graph build: rows == cols ==
+// the partition, self excluded, tiny partitions cyclic (graph_index.cpp:46-97).
+// Brute force (topk.cpp:12-30): rows = queries, cols = database.
+__global__ void __launch_bounds__(256) knn_kernel(const float* __restrict__ rowv, uint64_t nrows,
+                                                  const float* __restrict__ vec, uint64_t n,
+                                                  int dpad, int deg, bool build,
+                                                  uint32_t* __restrict__ adj,
+                                                  float* __restrict__ out_dists) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // transposed row / column chunks, then per-row survivors of this tile
   float (*xs)[TR] = reinterpret_cast<float (*)[TR]>(smem_raw);
@@ -73,7 +78,7 @@ __global__ void __launch_bounds__(256) knn_kernel(const float* __restrict__ vec,
         const int dd = d0 + ch * 4;
         float4 vx = make_float4(0.f, 0.f, 0.f, 0.f), vy = vx;
         if (dd < dpad) {
-          if (r0 + r < n) vx = *reinterpret_cast<const float4*>(vec + (r0 + r) * dpad + dd);
+          if (r0 + r < nrows) vx = *reinterpret_cast<const float4*>(rowv + (r0 + r) * dpad + dd);
           if (c0 + r < n) vy = *reinterpret_cast<const float4*>(vec + (c0 + r) * dpad + dd);
         }
         xs[ch * 4 + 0][r] = vx.x; xs[ch * 4 + 1][r] = vx.y;
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(256) knn_kernel(const float* __restrict__ vec,
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint64_t col = c0 + tx * 4 + j;
-        if (row < n && col < n && col != row) {
+        if (row < nrows && col < n && (!build || col != row)) {
           const uint64_t key = ((uint64_t)f2ord(acc[i][j]) << 32) | (uint32_t)col;
           if (key < cut) cbuf[rl][atomicAdd(&ccount[rl], 1)] = key;
         }
@@ -138,7 +143,15 @@ __global__ void __launch_bounds__(256) knn_kernel(const float* __restrict__ vec,
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const uint64_t row = r0 + warp * 8 + i;
-    if (row >= n) continue;
+    if (row >= nrows) continue;
+    if (!build) {  // brute force: the deg smallest (dist, id), k <= n checked on the host
+      if (lane < deg) {
+        adj[row * (uint64_t)deg + lane] = (uint32_t)top[i];
+        const uint32_t o = (uint32_t)(top[i] >> 32);
+        out_dists[row * (uint64_t)deg + lane] = __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+      }
+      continue;
+    }
     const uint64_t valid = n - 1 < (uint64_t)deg ? n - 1 : (uint64_t)deg;
     for (int j = 0; j < deg; ++j) {
       const int src = valid > 0 ? (int)((uint64_t)j % valid) : 0;
@@ -160,7 +173,22 @@ cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad
   cudaError_t e =
       cudaFuncSetAttribute(knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  knn_kernel<<<(unsigned)blocks, 256, smem, stream>>>(vectors, n, dpad, out_degree, adjacency);
+  knn_kernel<<<(unsigned)blocks, 256, smem, stream>>>(vectors, n, vectors, n, dpad, out_degree, true,
+                                                      adjacency, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_brute_force(const float* queries, uint64_t nq, const float* db, uint64_t n,
+                               int dpad, int k, uint32_t* out_ids, float* out_dists,
+                               cudaStream_t stream) {
+  if (k < 1 || k > MAXDEG || (uint64_t)k > n) return cudaErrorInvalidValue;
+  const uint64_t blocks = (nq + TR - 1) / TR;
+  const size_t smem = sizeof(float) * DC * (TR + TC) + sizeof(uint64_t) * TR * TC;
+  cudaError_t e =
+      cudaFuncSetAttribute(knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  knn_kernel<<<(unsigned)blocks, 256, smem, stream>>>(queries, nq, db, n, dpad, k, false, out_ids,
+                                                      out_dists);
   return cudaGetLastError();
 }
 

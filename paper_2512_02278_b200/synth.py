@@ -80,9 +80,14 @@ def build_index(ctx: Context, data: np.ndarray, clusters: int, out_degree: int =
     return BuiltIndex(cents, placement, ranks, out_degree, graphs)
 
 
-def brute_force_gt(data: np.ndarray, queries: np.ndarray, k: int, device: str = "cuda:0"):
-    """Exact top-k ids for recall (measurement only): fp32 expansion, exact on
-    integer data (< 2^24); ties broken by lower id like brute_force_topk."""
+def brute_force_gt(data: np.ndarray, queries: np.ndarray, k: int, device: str = "cuda:0",
+                   ctx=None):
+    """Exact top-k ids for recall@k (topk.cpp:12-30, ties by lower id): the
+    library's GPU brute force (dvsg_brute_force_topk) when k <= 32."""
+    if k <= 32:
+        from .api import Context
+        cx = ctx or Context(int(device.split(":")[1]) if ":" in device else 0)
+        return cx.brute_force_topk(data, queries, k)[0]
     import torch
     x = torch.from_numpy(data).to(device)
     xn = (x.double() ** 2).sum(1).float()

@@ -383,3 +383,16 @@ def test_odd_degrees_match_oracle(ctx, oracle, dg):
     want = oracle.beam_search(v, gids, adj, eo, q, 8, 24, 10, 8)
     got = _search(ctx, v, adj, q, dvs.SearchParams(8, 24, 10, 8, accum="f64"))
     _assert_same(got, want, True, f"dg={dg}")
+
+
+def test_brute_force_topk_matches_reference(ctx, golden, oracle):
+    g = golden("g2_siftlike.npz")  # truth from the reference's brute_force_topk
+    ids, d = ctx.brute_force_topk(g["vectors"], g["queries"], 10)
+    assert np.array_equal(ids, g["truth_ids"]) and np.array_equal(d, g["truth_dists"])
+    v = sift_like(5000, 48, 4, 77)  # many exact ties: (dist, id) order
+    q = sift_like(50, 48, 4, 78)
+    wi, wd = oracle.brute_force_topk(v, q, 32)
+    gi, gd = ctx.brute_force_topk(v, q, 32)
+    assert np.array_equal(gi, wi) and np.array_equal(gd, wd)
+    with pytest.raises(dvs.InvalidArgument):
+        ctx.brute_force_topk(v[:5], q, 6)
