@@ -163,6 +163,18 @@ dvsg_status dvsg_search_sharded_device(dvsg_ctx *ctx, const float *d_queries, ui
                                        float *d_out_dists, uint32_t *d_out_count,
                                        uint64_t *d_out_visited);
 
+/* Exchange algorithm of the node-sharded search (both exact):
+ *   0  bulk-synchronous (default): per phase, xg_expand pushes every query's
+ *      new candidates into the owners' inboxes, a peer-flag barrier, xg_score
+ *      scores them and pushes the keys back, a barrier (xchg_kernel.cu);
+ *   1  fused: one persistent kernel, per-CTA request/reply round trips
+ *      (shard_kernel.cu).
+ * Default from the environment (DVSG_SHARD_EXCHANGE=fused), else 0.  With the
+ * bulk exchange, dvsg_search_sharded_device is collective: every rank must
+ * call it with the same nq and params; dvsg_synchronize reports a rank that
+ * never reached a barrier (DVSG_EINTERNAL after 20 s). */
+dvsg_status dvsg_set_shard_exchange(dvsg_ctx *ctx, int mode);
+
 /* ---- routing and merge -------------------------------------------------- */
 
 /* assign_top_c, kmeans.cpp:243-280, on the GPU against the context's

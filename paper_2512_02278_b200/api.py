@@ -284,6 +284,11 @@ class Context:
         buf = ctypes.create_string_buffer(blob, len(blob))
         check(lib.dvsg_shard_connect(self._h, buf))
 
+    def set_shard_exchange(self, mode: str) -> None:
+        """'bulk' (bulk-synchronous phases, xchg_kernel.cu; default) or 'fused'
+        (per-CTA round trips, shard_kernel.cu); both exact."""
+        check(lib.dvsg_set_shard_exchange(self._h, {"bulk": 0, "fused": 1}[mode]))
+
     def shard_prepare(self) -> None:
         check(lib.dvsg_shard_prepare(self._h))
 

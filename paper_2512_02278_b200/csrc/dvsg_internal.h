@@ -88,6 +88,65 @@ cudaError_t launch_search_sharded(const SearchArgs& a, const ShardArgs& sh, int 
 // CTAs per rank the sharded kernel can keep resident for these args.
 int search_sharded_blocks_per_sm(const SearchArgs& a, int metric, int accum);
 
+// ---- node-sharded, bulk-synchronous frontier exchange (xchg_kernel.cu) ----
+// Same shard rule as above (node v on rank v / shard_rows).  Per phase every
+// rank's origins push their new candidate ids into the owners' inboxes, the
+// owners score them and push the keys back; a peer-flag barrier separates the
+// phases.  Each rank's comm arena (IPC-exported) holds:
+struct XgView {
+  const float* vec;    // this rank's shard rows: node v at vec + (v - lo) * dpad (owner side)
+  uint64_t lo;
+  unsigned* cursor;    // [2][nranks] inbox fill per origin, slot = phase & 1
+  unsigned* flags;     // [nranks] barrier epoch last published by each rank
+  float* qall;         // [nranks][wcap][dpad] every origin's queries (this wave)
+  uint64_t* inbox;     // [nranks][rstride] requests (qid << 32 | node) from each origin
+  uint64_t* reply;     // [nranks][rstride] keys scored by each owner, same index as its inbox
+};
+
+constexpr int kXgMaxRanks = 8;
+
+struct XgArgs {
+  const XgView* views;  // device array [nranks]
+  int nranks;
+  int rank_lo, rank_n;  // ranks this launch acts for (multi-GPU: self, 1; emulation: 0, R)
+  uint32_t wave_n[kXgMaxRanks];  // queries of each acting rank in this wave
+  uint32_t wcap;        // per-rank query capacity (state / qall stride)
+  uint32_t maxraw;      // max new candidates per query per phase
+  uint64_t rstride;     // wcap * maxraw
+  uint32_t shard_rows;  // S
+  int phase;            // 0: entry nodes, 1..iters: expansions, iters + 1: finalize
+  // origin state, [rank_n][wcap] (acting-rank relative)
+  uint64_t* pool;       // x cap
+  uint32_t* psize;
+  uint64_t* visited;
+  uint32_t* expd;
+  uint32_t* hash;       // x hsize
+  uint2* meta;          // x nranks: (inbox position, count) at each owner, last phase
+  // replicated graph
+  const uint32_t* adjacency;
+  const uint32_t* gids;
+  const uint32_t* entry;
+  uint32_t n;
+  int dim, dpad, dg, iters, beam, k, entry_count, cap, chp, hsize;
+  // outputs: acting rank rr's wave query j at [rr * out_stride + j]
+  uint32_t* out_ids;
+  float* out_dists;
+  uint32_t* out_count;
+  uint64_t* out_visited;
+  uint64_t out_stride;
+  unsigned long long* work_counter;
+  unsigned long long* stats;  // [0] units, [1] visited, [2] expanded
+  int* err;
+  int expand_ctas, score_ctas;  // > 0: CTAs per SM of each kernel (room for the other lane)
+};
+
+size_t xg_expand_smem_bytes(int cap, int chp, int beam, int maxraw);
+cudaError_t launch_xg_expand(const XgArgs& a, int num_sms, cudaStream_t stream);
+cudaError_t launch_xg_score(const XgArgs& a, int metric, int accum, int num_sms, cudaStream_t stream);
+// Peer-flag barrier over all ranks (one thread); sets bit 3 of *err after a 20 s timeout.
+cudaError_t launch_xg_barrier(const XgView* views, int nranks, int me, unsigned epoch, int* err,
+                              cudaStream_t stream);
+
 // Launch K1 (search_kernel.cu).  Returns a cudaError_t.
 // max_grid > 0 caps the persistent grid (one global hash region per CTA).
 cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sms,

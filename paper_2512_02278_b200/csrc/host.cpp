@@ -95,6 +95,17 @@ struct DevBuf {
   }
 };
 
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
+bool ids_increasing(const uint32_t* g, uint64_t n) {
+  for (uint64_t i = 1; i < n; ++i)
+    if (g[i] <= g[i - 1]) return false;
+  return true;
+}
+
 bool finite_all(const float* x, uint64_t n) {
   for (uint64_t i = 0; i < n; ++i)
     if (!std::isfinite(x[i])) return false;
@@ -115,6 +126,7 @@ struct dvsg_ctx {
   DevBuf<float> vec;
   DevBuf<uint32_t> adj, gids, entry;
   std::vector<dvsg::PartDesc> parts;
+  std::vector<char> part_mono;     // global ids strictly increasing in local id (per part)
   DevBuf<dvsg::PartDesc> d_parts;
   bool parts_dirty = true;
   // routing table
@@ -153,7 +165,26 @@ struct dvsg_ctx {
     unsigned char* arena = nullptr;            // own comm arena (IPC-exported)
     std::vector<unsigned char*> peers;         // every rank's arena (own included)
     bool connected = false;
+    size_t xg_off = 0, xg_bytes = 0;           // bulk-exchange region of the arena
   } sh;
+  // bulk-synchronous exchange (xchg_kernel.cu): origin state + emulation arenas
+  struct Xg {
+    DevBuf<uint64_t> pool, visited;
+    DevBuf<uint32_t> psize, expd, hash;
+    DevBuf<uint2> meta;
+    DevBuf<unsigned char> emu_arena;
+    DevBuf<float> emu_q;
+    DevBuf<dvsg::XgView> d_views;
+    DevBuf<unsigned long long> counters;
+    DevBuf<int> err;
+    unsigned epoch[4] = {0, 0, 0, 0};
+    bool kind_recorded[2][4] = {};
+    bool issued = false;
+  } xg;
+  cudaStream_t xg_streams[4] = {};   // lanes 1.. of the bulk exchange (lane 0: stream)
+  cudaEvent_t xg_ev[4] = {};
+  cudaEvent_t xg_kind_ev[2][4] = {};
+  int shard_exchange = -1;                     // 0 bulk (default), 1 fused; -1: env DVSG_SHARD_EXCHANGE
   DevBuf<unsigned char> emu_arena;             // emulation: all virtual ranks' arenas
   DevBuf<dvsg::ShardView> d_views;
   DevBuf<uint32_t> iota_q, zero_p;
@@ -266,6 +297,19 @@ K1Shape k1_shape(dvsg_ctx* c, const dvsg_search_params* p, uint64_t nmax, bool a
   K1Shape k{};
   k.cap = std::max<uint64_t>(4ull * (uint64_t)p->k, 2ull * (uint64_t)p->iterations * (uint64_t)p->beam_width);
   if (k.cap > (1ull << 20)) fail(DVSG_EINVAL, "beam_search: candidate pool capacity %llu exceeds the device limit", (unsigned long long)k.cap);
+  // Exact pool truncation.  The frontier of iteration t is the first w
+  // unexpanded entries, and at most t*w entries are expanded, so every pick
+  // sits at a position < I*w; entries only ever move down.  Hence keeping
+  // the first max(I*w, k) entries instead of cap = max(4k, 2*I*w)
+  // (graph_index.cpp:127-129) picks the same frontiers, scores the same
+  // vectors (same visited counter) and holds the same first k -- and when
+  // global ids increase with local ids the final (dist, gid) order equals the
+  // pool's (dist, local) order, so no tie beyond position k can enter the
+  // top k either.  Halves the pool, the survivors to sort and the merges.
+  static const bool trunc_env = env_u64("DVSG_POOL_TRUNC", 1) != 0;
+  bool mono = trunc_env && !c->part_mono.empty();
+  for (char m : c->part_mono) mono = mono && m;
+  if (mono) k.cap = std::max<uint64_t>((uint64_t)p->k, (uint64_t)p->iterations * (uint64_t)p->beam_width);
   // visited never exceeds min(n_max, entries + I*w*dg)
   const uint64_t entries = std::min<uint64_t>((uint64_t)p->entry_count, nmax);
   const uint64_t bound = std::min<uint64_t>(nmax, entries + (uint64_t)p->iterations * (uint64_t)p->beam_width * (uint64_t)c->dg);
@@ -507,6 +551,274 @@ void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uin
   c->launches += 1;
 }
 
+// ---- node-sharded search, bulk-synchronous exchange (xchg_kernel.cu) -------
+constexpr size_t kXgHeader = 256;  // cursor [2][8] u32 @0, flags [8] u32 @64
+constexpr int kXgLanes = 4;
+
+size_t xg_region_bytes(int nranks, uint64_t wcap, uint64_t maxraw, int dpad) {
+  size_t b = kXgHeader;
+  b += (size_t)nranks * wcap * (uint64_t)dpad * 4;
+  b = (b + 255) & ~(size_t)255;
+  b += 2 * (size_t)nranks * wcap * maxraw * 8;
+  return b;
+}
+
+dvsg::XgView xg_view(unsigned char* region, const float* vec, uint64_t lo, int nranks, uint64_t wcap,
+                     uint64_t maxraw, int dpad) {
+  dvsg::XgView v{};
+  v.vec = vec;
+  v.lo = lo;
+  v.cursor = reinterpret_cast<unsigned*>(region);
+  v.flags = reinterpret_cast<unsigned*>(region + 64);
+  size_t off = kXgHeader;
+  v.qall = reinterpret_cast<float*>(region + off);
+  off += (size_t)nranks * wcap * (uint64_t)dpad * 4;
+  off = (off + 255) & ~(size_t)255;
+  v.inbox = reinterpret_cast<uint64_t*>(region + off);
+  off += (size_t)nranks * wcap * maxraw * 8;
+  v.reply = reinterpret_cast<uint64_t*>(region + off);
+  return v;
+}
+
+void xg_check(dvsg_ctx* c) {
+  if (!c->xg.issued) return;
+  int err = 0;
+  cuda_check(cudaMemcpy(&err, c->xg.err.p, sizeof err, cudaMemcpyDeviceToHost), "sharded err");
+  c->xg.issued = false;
+  if (err & 8) fail(DVSG_EINTERNAL, "sharded search: a peer rank did not reach the exchange barrier (20 s)");
+}
+
+// emulate: all R ranks on this device (queries split evenly, rank r origin of
+// [r*upr, (r+1)*upr)); else this rank's nq queries, every rank concurrently.
+// The rank's queries are processed in waves; L lanes (streams, each with its
+// own comm region, state slice and barrier epoch) run waves concurrently,
+// offset by half a phase so one lane's xg_expand (latency bound) overlaps the
+// other lane's xg_score (HBM bound).
+void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64_t nq, int dim,
+                 const dvsg_search_params* p, uint32_t* d_ids, float* d_dists, uint32_t* d_count,
+                 uint64_t* d_visited) {
+  validate_params(p);
+  if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
+  if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
+  if (nranks < 1 || nranks > dvsg::kXgMaxRanks) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
+  if (c->dpad > 768) fail(DVSG_EINVAL, "sharded search: dim above 768 not supported");
+  if (nq == 0) return;
+  sync_parts(c);
+  const int R = nranks;
+  const uint64_t n = c->sh.active ? c->sh.n_total : c->parts[0].n;
+  const K1Shape k = k1_shape(c, p, n, false);
+  const uint64_t maxraw = std::max<uint64_t>(std::min<uint64_t>((uint64_t)p->entry_count, n),
+                                             (uint64_t)p->beam_width * (uint64_t)c->dg);
+  const size_t smem = dvsg::xg_expand_smem_bytes((int)k.cap, (int)k.chp, p->beam_width, (int)maxraw);
+  if (smem > c->smem_optin) fail(DVSG_EINVAL, "sharded search: beam x degree / entry_count too large (%llu new candidates per phase)", (unsigned long long)maxraw);
+  const uint64_t S = emulate ? (n + (uint64_t)R - 1) / (uint64_t)R : c->sh.shard_rows;
+  const uint64_t upr = emulate ? (nq + (uint64_t)R - 1) / (uint64_t)R : nq;
+  const int rank_n = emulate ? R : 1;
+  const int me = emulate ? 0 : c->sh.rank;
+  auto rank_count = [&](int r) -> uint64_t {
+    if (!emulate) return nq;
+    const uint64_t lo = std::min<uint64_t>(nq, (uint64_t)r * upr);
+    return std::min<uint64_t>(nq, lo + upr) - lo;
+  };
+  if (!emulate) {
+    if (!c->sh.connected) fail(DVSG_EINVAL, "sharded search: call dvsg_shard_init and dvsg_shard_connect first");
+    if (nranks != c->sh.nranks) fail(DVSG_EINVAL, "sharded search: nranks %d != %d", nranks, c->sh.nranks);
+  }
+  // lanes and wave size (comm region + origin state budgets, split per lane)
+  const int L = (int)std::max<uint64_t>(1, std::min<uint64_t>(kXgLanes, env_u64("DVSG_XG_LANES", 2)));
+  const uint64_t comm_q = (uint64_t)R * ((uint64_t)c->dpad * 4 + 16 * maxraw);
+  const uint64_t state_q = k.cap * 8 + k.hsize * 4 + 16 + 8 * (uint64_t)R;
+  const size_t lane_bytes = emulate ? 0 : ((c->sh.xg_bytes / (size_t)L) & ~(size_t)4095);
+  uint64_t wmax = upr;
+  if (emulate) {
+    wmax = std::min<uint64_t>(wmax, std::max<uint64_t>(1, (env_u64("DVSG_XG_EMU_MB", 2048) << 20) / ((uint64_t)L * R * comm_q)));
+  } else {
+    const uint64_t room = lane_bytes > kXgHeader + 512 ? (lane_bytes - kXgHeader - 512) / comm_q : 0;
+    if (room < 1) fail(DVSG_EINVAL, "sharded search: comm arena too small for one query");
+    wmax = std::min<uint64_t>(wmax, room);
+  }
+  wmax = std::min<uint64_t>(wmax, std::max<uint64_t>(1, (env_u64("DVSG_XG_STATE_MB", 16384) << 20) / ((uint64_t)L * rank_n * state_q)));
+  const uint64_t wlim = env_u64("DVSG_XG_WAVE", 0);
+  if (wlim) wmax = std::min<uint64_t>(wmax, wlim);
+  wmax = std::min<uint64_t>(wmax, 1ull << 30);
+  // equal waves, a multiple of L of them (every lane busy)
+  uint64_t nwaves = (upr + wmax - 1) / wmax;
+  if (L > 1) nwaves = (nwaves + L - 1) / (uint64_t)L * (uint64_t)L;
+  const uint64_t wcap = (upr + nwaves - 1) / nwaves;
+  const uint64_t rstride = wcap * maxraw;
+
+  auto& x = c->xg;
+  const uint64_t st_n = (uint64_t)L * rank_n * wcap;
+  x.pool.reserve(st_n * k.cap, c->stream);
+  x.visited.reserve(st_n, c->stream);
+  x.psize.reserve(st_n, c->stream);
+  x.expd.reserve(st_n, c->stream);
+  x.hash.reserve(st_n * k.hsize, c->stream);
+  x.meta.reserve(st_n * (uint64_t)R, c->stream);
+  x.counters.reserve((size_t)L * ((size_t)p->iterations + 2), c->stream);
+  x.err.reserve(1, c->stream);
+  cuda_check(cudaMemsetAsync(x.err.p, 0, sizeof(int), c->stream), "err reset");
+
+  // views: [lane][rank]
+  std::vector<dvsg::XgView> views((size_t)L * R);
+  if (emulate) {
+    const size_t rb = xg_region_bytes(R, wcap, maxraw, c->dpad);
+    x.emu_arena.reserve(rb * (size_t)R * L, c->stream);
+    x.emu_q.reserve((size_t)L * R * wcap * (uint64_t)c->dpad, c->stream);
+    for (int l = 0; l < L; ++l)
+      for (int r = 0; r < R; ++r) {
+        unsigned char* reg = x.emu_arena.p + rb * ((size_t)l * R + r);
+        cuda_check(cudaMemsetAsync(reg, 0, kXgHeader, c->stream), "xg header reset");
+        auto& v = views[(size_t)l * R + r];
+        v = xg_view(reg, c->vec.p + (uint64_t)r * S * (uint64_t)c->dpad, (uint64_t)r * S, R, wcap, maxraw, c->dpad);
+        v.qall = x.emu_q.p + (size_t)l * R * wcap * (uint64_t)c->dpad;  // one copy stands in for every owner's
+      }
+  } else {
+    for (int l = 0; l < L; ++l)
+      for (int r = 0; r < R; ++r)
+        views[(size_t)l * R + r] = xg_view(c->sh.peers[(size_t)r] + c->sh.xg_off + (size_t)l * lane_bytes,
+                                           r == me ? c->vec.p : nullptr, (uint64_t)r * S, R, wcap, maxraw, c->dpad);
+  }
+  x.d_views.reserve(views.size(), c->stream);
+  cuda_check(cudaMemcpyAsync(x.d_views.p, views.data(), views.size() * sizeof(dvsg::XgView), cudaMemcpyHostToDevice, c->stream), "views");
+
+  dvsg::SearchArgs ka = k1_args(c, p, k, d_q, nq, dim, nullptr, nullptr, nq, d_ids, d_dists, d_count, d_visited);
+  dvsg::XgArgs base{};
+  base.nranks = R;
+  base.rank_lo = me;
+  base.rank_n = rank_n;
+  base.wcap = (uint32_t)wcap;
+  base.maxraw = (uint32_t)maxraw;
+  base.rstride = rstride;
+  base.shard_rows = (uint32_t)S;
+  base.adjacency = c->adj.p;
+  base.gids = c->gids.p;
+  base.entry = c->entry.p;
+  base.n = (uint32_t)n;
+  base.dim = dim;
+  base.dpad = c->dpad;
+  base.dg = c->dg;
+  base.iters = p->iterations;
+  base.beam = p->beam_width;
+  base.k = p->k;
+  base.entry_count = p->entry_count;
+  base.cap = (int)k.cap;
+  base.chp = (int)k.chp;
+  base.hsize = (int)k.hsize;
+  base.out_stride = emulate ? upr : 0;
+  base.stats = ka.stats;
+  base.err = x.err.p;
+  base.expand_ctas = (int)env_u64("DVSG_XG_EXPAND_CTAS", L > 1 ? 2 : 0);
+  base.score_ctas = (int)env_u64("DVSG_XG_SCORE_CTAS", L > 1 ? 2 : 0);
+  dvsg::XgArgs la[kXgLanes];
+  cudaStream_t ls[kXgLanes];
+  for (int l = 0; l < L; ++l) {
+    la[l] = base;
+    la[l].views = x.d_views.p + (size_t)l * R;
+    const uint64_t so = (uint64_t)l * rank_n * wcap;
+    la[l].pool = x.pool.p + so * k.cap;
+    la[l].psize = x.psize.p + so;
+    la[l].visited = x.visited.p + so;
+    la[l].expd = x.expd.p + so;
+    la[l].hash = x.hash.p + so * k.hsize;
+    la[l].meta = x.meta.p + so * (uint64_t)R;
+    ls[l] = l == 0 ? c->stream : c->xg_streams[l];
+  }
+  // lane streams start after everything queued so far on the compute stream
+  cuda_check(cudaEventRecord(c->xg_ev[0], c->stream), "event");
+  for (int l = 1; l < L; ++l) cuda_check(cudaStreamWaitEvent(ls[l], c->xg_ev[0], 0), "wait");
+
+  auto barrier = [&](int l) {
+    if (emulate) return;  // stream order is the barrier
+    x.epoch[l] += 1;
+    cuda_check(dvsg::launch_xg_barrier(la[l].views, R, me, x.epoch[l], x.err.p, ls[l]), "xg barrier");
+    c->launches += 1;
+  };
+  // half-phase offset between lanes: lane l's kernel of a kind waits for
+  // lane l-1's kernel of the same kind (and lane 0 for the last lane's)
+  const bool stagger = L > 1 && env_u64("DVSG_XG_STAGGER", 1) != 0;
+  auto after = [&](int l, int kind) {  // kind 0 expand, 1 score
+    if (!stagger) return;
+    const int prev = (l + L - 1) % L;
+    cudaEvent_t e = c->xg_kind_ev[kind][prev];
+    if (x.kind_recorded[kind][prev]) cuda_check(cudaStreamWaitEvent(ls[l], e, 0), "wait");
+  };
+  auto done = [&](int l, int kind) {
+    if (!stagger) return;
+    cuda_check(cudaEventRecord(c->xg_kind_ev[kind][l], ls[l]), "event");
+    x.kind_recorded[kind][l] = true;
+  };
+  for (int l = 0; l < kXgLanes; ++l) x.kind_recorded[0][l] = x.kind_recorded[1][l] = false;
+
+  if (c->timing) cudaEventRecord(c->ev[0], c->stream);
+  for (uint64_t w0 = 0; w0 < nwaves; w0 += (uint64_t)L) {
+    for (int l = 0; l < L; ++l) {
+      auto& a = la[l];
+      const uint64_t off = (w0 + (uint64_t)l) * wcap;
+      for (int rr = 0; rr < rank_n; ++rr) {
+        const uint64_t cnt = rank_count(me + rr);
+        a.wave_n[rr] = (uint32_t)(cnt > off ? std::min<uint64_t>(wcap, cnt - off) : 0);
+      }
+      // each origin's wave queries into every owner's qall[origin] (padded rows)
+      for (int rr = 0; rr < rank_n; ++rr) {
+        if (!a.wave_n[rr]) continue;
+        const int o = me + rr;
+        const float* src = d_q + ((emulate ? (uint64_t)o * upr : 0) + off) * (uint64_t)dim;
+        for (int r = 0; r < (emulate ? 1 : R); ++r) {
+          float* dst = views[(size_t)l * R + r].qall + (uint64_t)o * wcap * (uint64_t)c->dpad;
+          cuda_check(cudaMemcpy2DAsync(dst, (size_t)c->dpad * 4, src, (size_t)dim * 4, (size_t)dim * 4,
+                                       a.wave_n[rr], cudaMemcpyDefault, ls[l]), "push queries");
+        }
+      }
+      a.out_ids = d_ids + off * (uint64_t)p->k;
+      a.out_dists = d_dists + off * (uint64_t)p->k;
+      a.out_count = d_count + off;
+      a.out_visited = d_visited + off;
+      unsigned long long* ctr = x.counters.p + (size_t)l * ((size_t)p->iterations + 2);
+      cuda_check(cudaMemsetAsync(ctr, 0, ((size_t)p->iterations + 2) * sizeof(unsigned long long), ls[l]), "counters");
+      barrier(l);  // every owner holds this wave's queries
+    }
+    for (int ph = 0; ph <= p->iterations + 1; ++ph) {
+      for (int l = 0; l < L; ++l) {
+        auto& a = la[l];
+        a.phase = ph;
+        a.work_counter = x.counters.p + (size_t)l * ((size_t)p->iterations + 2) + ph;
+        after(l, 0);
+        cuda_check(dvsg::launch_xg_expand(a, c->num_sms, ls[l]), "xg expand");
+        done(l, 0);
+        c->launches += 1;
+        if (ph > p->iterations) continue;  // finalize pass
+        barrier(l);  // requests delivered
+        after(l, 1);
+        cuda_check(dvsg::launch_xg_score(a, p->metric, p->accum, c->num_sms, ls[l]), "xg score");
+        done(l, 1);
+        c->launches += 1;
+        // this phase's inbox cursors are free again (next used two barriers later)
+        for (int rr = 0; rr < rank_n; ++rr)
+          cuda_check(cudaMemsetAsync(views[(size_t)l * R + me + rr].cursor + (ph & 1) * R, 0, (size_t)R * 4, ls[l]), "cursor reset");
+        barrier(l);  // replies delivered
+      }
+    }
+  }
+  for (int l = 1; l < L; ++l) {
+    cuda_check(cudaEventRecord(c->xg_ev[l], ls[l]), "event");
+    cuda_check(cudaStreamWaitEvent(c->stream, c->xg_ev[l], 0), "join");
+  }
+  if (c->timing) {
+    cudaEventRecord(c->ev[1], c->stream);
+    c->timing_pending = 1;
+  }
+  x.issued = true;
+}
+
+bool use_bulk_exchange(dvsg_ctx* c) {
+  if (c->shard_exchange < 0) {
+    const char* e = std::getenv("DVSG_SHARD_EXCHANGE");
+    c->shard_exchange = (e && std::strcmp(e, "fused") == 0) ? 1 : 0;
+  }
+  return c->shard_exchange == 0;
+}
+
 template <class T>
 T* stage(DevBuf<T>& b, const T* host, size_t n, cudaStream_t s) {
   b.reserve(std::max<size_t>(n, 1), s);
@@ -687,6 +999,10 @@ dvsg_status dvsg_create(int device, dvsg_ctx** out) {
     c->smem_optin = prop.sharedMemPerBlockOptin;
     cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking), "stream");
+    for (int l = 1; l < 4; ++l) cuda_check(cudaStreamCreateWithFlags(&c->xg_streams[l], cudaStreamNonBlocking), "stream");
+    for (auto& e : c->xg_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& row : c->xg_kind_ev)
+      for (auto& e : row) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
     for (auto& e : c->mb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     *out = c.release();
@@ -705,6 +1021,10 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     for (auto& e : c->mb_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm);
+    for (int l = 1; l < 4; ++l) cudaStreamDestroy(c->xg_streams[l]);
+    for (auto& e : c->xg_ev) cudaEventDestroy(e);
+    for (auto& row : c->xg_kind_ev)
+      for (auto& e : row) cudaEventDestroy(e);
     delete c;
   });
 }
@@ -715,6 +1035,7 @@ dvsg_status dvsg_synchronize(dvsg_ctx* c) {
   return guarded([&] {
     set_device(c);
     cuda_check(cudaStreamSynchronize(c->stream), "synchronize");
+    xg_check(c);
   });
 }
 
@@ -723,6 +1044,7 @@ dvsg_status dvsg_index_reset(dvsg_ctx* c) {
     set_device(c);
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
     c->parts.clear();
+    c->part_mono.clear();
     c->rows = 0;
     c->dim = c->dpad = c->dg = 0;
     c->clusters = 0;
@@ -813,6 +1135,7 @@ dvsg_status dvsg_load_partition(dvsg_ctx* c, uint32_t cluster, uint64_t n, int d
     cuda_check(cudaMemcpy(c->gids.p + r0, global_ids, n * 4, cudaMemcpyHostToDevice), "gids H2D");
     cuda_check(cudaMemcpy(c->entry.p + r0, entry_order, n * 4, cudaMemcpyHostToDevice), "entry H2D");
     c->parts.push_back(dvsg::PartDesc{r0, (uint32_t)n, cluster});
+    c->part_mono.push_back(ids_increasing(global_ids, n));
     c->rows = r1;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = c->anchors_dirty = true;
   });
@@ -916,12 +1239,14 @@ dvsg_status dvsg_beam_search_sharded_emulated(dvsg_ctx* c, int nranks, const flo
     c->u_dists.reserve(nq * k, c->stream);
     c->u_count.reserve(nq, c->stream);
     c->u_visited.reserve(nq, c->stream);
-    search_sharded(c, true, nranks, d_q, nq, dim, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
+    if (use_bulk_exchange(c)) search_xchg(c, true, nranks, d_q, nq, dim, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
+    else search_sharded(c, true, nranks, d_q, nq, dim, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
     cuda_check(cudaMemcpyAsync(out_ids, c->u_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaMemcpyAsync(out_dists, c->u_dists.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaMemcpyAsync(out_count, c->u_count.p, nq * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaMemcpyAsync(out_visited, c->u_visited.p, nq * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaStreamSynchronize(c->stream), "sharded search");
+    xg_check(c);
     read_timings(c, false);
   });
 }
@@ -943,6 +1268,7 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
       if (adjacency[i] >= n_total) fail(DVSG_EFORMAT, "index file: neighbor id out of range");
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
     c->parts.clear();
+    c->part_mono.clear();
     c->dim = dim;
     c->dpad = (dim + 3) & ~3;
     c->dg = out_degree;
@@ -966,6 +1292,7 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
     }
     cuda_check(cudaMemcpy(c->entry.p, entry_order, n_total * 4, cudaMemcpyHostToDevice), "entry H2D");
     c->parts.push_back(dvsg::PartDesc{0, (uint32_t)n_total, 0});
+    c->part_mono.push_back(global_ids ? ids_increasing(global_ids, n_total) : 1);
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
     auto& sh = c->sh;
     if (sh.arena) cudaFree(sh.arena);
@@ -978,8 +1305,13 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
     sh.gpr_max = 8 * c->num_sms;
     sh.ring_cap = (uint32_t)pow2_at_least((uint64_t)nranks * sh.gpr_max);
     sh.arena_bytes = shard_arena_bytes(nranks, sh.gpr_max, sh.ring_cap, c->dpad);
+    // + the bulk-exchange region (queries, inboxes, replies of one wave)
+    sh.xg_off = (sh.arena_bytes + 4095) & ~(size_t)4095;
+    sh.xg_bytes = (size_t)env_u64("DVSG_XG_ARENA_MB", 16384) << 20;
+    sh.arena_bytes = sh.xg_off + sh.xg_bytes;
     cuda_check(cudaMalloc(&sh.arena, sh.arena_bytes), "arena");
-    cuda_check(cudaMemset(sh.arena, 0, sh.arena_bytes), "arena reset");
+    cuda_check(cudaMemset(sh.arena, 0, sh.xg_off + kXgHeader), "arena reset");
+    for (auto& e : c->xg.epoch) e = 0;
   });
 }
 
@@ -1018,8 +1350,9 @@ dvsg_status dvsg_shard_prepare(dvsg_ctx* c) {
   return guarded([&] {
     set_device(c);
     if (!c->sh.active) fail(DVSG_EINVAL, "shard_prepare: call dvsg_shard_init first");
-    cuda_check(cudaMemsetAsync(c->sh.arena, 0, c->sh.arena_bytes, c->stream), "arena reset");
+    cuda_check(cudaMemsetAsync(c->sh.arena, 0, c->sh.xg_off + kXgHeader, c->stream), "arena reset");
     cuda_check(cudaStreamSynchronize(c->stream), "arena reset");
+    for (auto& e : c->xg.epoch) e = 0;
   });
 }
 
@@ -1028,7 +1361,8 @@ dvsg_status dvsg_search_sharded_device(dvsg_ctx* c, const float* d_queries, uint
                                        float* d_out_dists, uint32_t* d_out_count, uint64_t* d_out_visited) {
   return guarded([&] {
     set_device(c);
-    search_sharded(c, false, c->sh.nranks, d_queries, nq, dim, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
+    if (use_bulk_exchange(c)) search_xchg(c, false, c->sh.nranks, d_queries, nq, dim, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
+    else search_sharded(c, false, c->sh.nranks, d_queries, nq, dim, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
   });
 }
 
@@ -1244,6 +1578,13 @@ dvsg_status dvsg_brute_force_topk(dvsg_ctx* c, const float* db, uint64_t n, int 
   });
 }
 
+dvsg_status dvsg_set_shard_exchange(dvsg_ctx* c, int mode) {
+  return guarded([&] {
+    if (mode != 0 && mode != 1) fail(DVSG_EINVAL, "set_shard_exchange: mode %d (0 bulk, 1 fused)", mode);
+    c->shard_exchange = mode;
+  });
+}
+
 dvsg_status dvsg_set_timing(dvsg_ctx* c, int enabled) {
   return guarded([&] { c->timing = enabled != 0; });
 }
@@ -1377,6 +1718,7 @@ dvsg_status dvsg_load_index_file(dvsg_ctx* c, const char* path, int rank) {
 
     // all structural checks passed: reset and upload the owned partitions
     c->parts.clear();
+    c->part_mono.clear();
     c->rows = 0;
     c->dim = c->dpad = c->dg = 0;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;

@@ -218,10 +218,10 @@ void sort_keys(uint64_t* s, int n, int tid) {
 }
 
 // out[0..outn) = first outn of merge(A[0..na), B[0..nb)); keys unique.
-// Merge path: each thread owns a contiguous slice of the output.
+// Merge path: each of nthreads threads owns a contiguous slice of the output.
 __device__ __forceinline__ void merge_path(const uint64_t* A, int na, const uint64_t* B, int nb,
-                                           uint64_t* out, int outn, int tid) {
-  const int per = (outn + kThreads - 1) / kThreads;
+                                           uint64_t* out, int outn, int tid, int nthreads = kThreads) {
+  const int per = (outn + nthreads - 1) / nthreads;
   const int o0 = min(tid * per, outn), o1 = min(o0 + per, outn);
   if (o0 >= o1) return;
   int lo = max(0, o0 - nb), hi = min(o0, na);
@@ -234,6 +234,62 @@ __device__ __forceinline__ void merge_path(const uint64_t* A, int na, const uint
     const bool takeA = ib >= nb || (ia < na && A[ia] < B[ib]);
     out[o] = takeA ? A[ia++] : B[ib++];
   }
+}
+
+// One warp sorts s[0..n) (n <= 32 * KPT) in registers; no block barrier.
+template <int KPT>
+__device__ __forceinline__ void warp_sort_slice(uint64_t* s, int n, int lane) {
+  uint64_t x[KPT];
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int e = lane * KPT + r;
+    x[r] = e < n ? s[e] : ~0ull;
+  }
+  bitonic_regs<KPT, 32>(x, lane, nullptr);
+#pragma unroll
+  for (int r = 0; r < KPT; ++r) {
+    const int e = lane * KPT + r;
+    if (e < n) s[e] = x[r];
+  }
+}
+
+// Sort s[0..n) (n <= 2048, block-uniform call): every warp sorts one eighth
+// in registers (bitonic, shuffles only), then three merge-path levels
+// ping-pong between s and tmp (>= n entries).  O(n log n) compare work
+// instead of the full block bitonic's O(n log^2 n) with smem stages.
+// Returns the buffer holding the sorted keys.
+__device__ __forceinline__ uint64_t* sort_runs(uint64_t* s, int n, uint64_t* tmp, int tid) {
+  if (n <= 128) {
+    sort_keys(s, n, tid);
+    return s;
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+  const int L = (n + kWarps - 1) / kWarps;  // <= 256
+  const int base = warp * L;
+  const int cnt = n - base < 0 ? 0 : (n - base < L ? n - base : L);
+  if (L <= 64) warp_sort_slice<2>(s + base, cnt, lane);
+  else if (L <= 128) warp_sort_slice<4>(s + base, cnt, lane);
+  else warp_sort_slice<8>(s + base, cnt, lane);
+  __syncthreads();
+  uint64_t* src = s;
+  uint64_t* dst = tmp;
+  int Lr = L;
+#pragma unroll 1
+  for (int pairs = kWarps / 2; pairs >= 1; pairs >>= 1) {
+    const int tpp = kThreads / pairs;
+    const int i = tid / tpp, t = tid - i * tpp;
+    const int a0 = i * 2 * Lr;
+    const int na = n - a0 < 0 ? 0 : (n - a0 < Lr ? n - a0 : Lr);
+    const int b0 = a0 + Lr;
+    const int nb = n - b0 < 0 ? 0 : (n - b0 < Lr ? n - b0 : Lr);
+    merge_path(src + a0, na, src + b0, nb, dst + a0, na + nb, t, tpp);
+    __syncthreads();
+    uint64_t* x = src;
+    src = dst;
+    dst = x;
+    Lr *= 2;
+  }
+  return src;
 }
 
 // U partial sums per lane -> lane holds the full sum of vector

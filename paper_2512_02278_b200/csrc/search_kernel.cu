@@ -34,6 +34,10 @@
 namespace dvsg {
 namespace {
 
+#ifndef DVSG_K1_SORT_RUNS
+#define DVSG_K1_SORT_RUNS 0
+#endif
+
 // VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
 // FULL: dpad == 128 * VPL (every lane holds real dimensions; no bound check).
 template <int VPL, typename ACC, int METRIC, bool FULL>
@@ -251,9 +255,17 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           atomicAdd(a.stats + 6 + (it < 0 ? 0 : (it < 1 ? 1 : 2)), (unsigned long long)S);
         }
 #endif
+#if DVSG_K1_SORT_RUNS
+        // warp-sorted runs + merge levels, ping-pong through cand (free after scoring)
+        const uint64_t* sorted = surv;
+        if (S <= kChunk / 2) sorted = sort_runs(surv, S, reinterpret_cast<uint64_t*>(cand), tid);
+        else sort_keys(surv, S, tid);
+#else
         sort_keys(surv, S, tid);
+        const uint64_t* sorted = surv;
+#endif
         const int outn = P + S < a.cap ? P + S : a.cap;
-        merge_path(pool, P, surv, S, pool_alt, outn, tid);
+        merge_path(pool, P, sorted, S, pool_alt, outn, tid);
         __syncthreads();
         {
           uint64_t* t = pool;

@@ -1,4 +1,4 @@
-"""K1 vs node-sharded K1 with R ranks emulated on one GPU (protocol overhead
+"""K1 vs node-sharded search (bulk and fused exchange) with R ranks emulated on one GPU (protocol overhead
 without NVLink): K1 event time for the bench workload, plus parity."""
 import os
 import sys
@@ -20,8 +20,11 @@ ref = None
 for _ in range(2):
     ref = ctx.beam_search(0, queries, p)
 print("unsharded K1 ms", round(ctx.last_timings()["search_ms"], 2), flush=True)
-for R in [1, 2, 4, 8]:
-    for _ in range(2):
-        got = ctx.beam_search_sharded_emulated(R, queries, p)
-    same = all(np.array_equal(a, b) for a, b in zip(got, ref))
-    print(f"emulated R={R} K1 ms", round(ctx.last_timings()["search_ms"], 2), "identical", same, flush=True)
+modes = os.environ.get("EXCHANGES", "bulk,fused").split(",")
+for mode in modes:
+    ctx.set_shard_exchange(mode)
+    for R in [int(r) for r in os.environ.get("RANKS", "1,2,4,8").split(",")]:
+        for _ in range(2):
+            got = ctx.beam_search_sharded_emulated(R, queries, p)
+        same = all(np.array_equal(a, b) for a, b in zip(got, ref))
+        print(f"{mode} emulated R={R} ms", round(ctx.last_timings()["search_ms"], 2), "identical", same, flush=True)

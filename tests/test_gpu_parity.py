@@ -84,6 +84,32 @@ def test_search_matches_oracle_fresh(ctx, oracle, n, dim, dg, I, w, k, E):
     _assert_same(got, want, True, (n, dim))
 
 
+@pytest.mark.parametrize("gid_order", ["increasing", "shuffled"])
+@pytest.mark.parametrize("I,w,k,E", [(6, 16, 10, 16), (2, 4, 10, 4), (3, 8, 50, 8), (1, 2, 5, 2)])
+def test_pool_truncation_exact_under_ties(ctx, oracle, gid_order, I, w, k, E):
+    """Tiny-integer coordinates (many equal distances): the pool kept at
+    max(I*w, k) (increasing gids) or at the reference cap (shuffled gids)
+    gives the reference's ids, dists and visited counters."""
+    n, dim = 1500, 6
+    rng = np.random.default_rng(5)
+    v = rng.integers(0, 4, size=(n, dim)).astype(np.float32)
+    adj = oracle.build_graph(v, 12)
+    eo = oracle.compute_entry_order(v)
+    q = rng.integers(0, 4, size=(80, dim)).astype(np.float32)
+    gids = (3 + 2 * np.arange(n)).astype(np.uint32)
+    if gid_order == "shuffled":
+        gids = rng.permutation(gids).astype(np.uint32)
+    want = oracle.beam_search(v, gids, adj, eo, q, I, w, k, E)
+    for accum in ("f64", "f32"):
+        got = _search(ctx, v, adj, q, dvs.SearchParams(I, w, k, E, accum=accum), gids)
+        _assert_same(got, want, True, (gid_order, accum))
+    ctx.reset()
+    ctx._single_key = None
+    ctx.load_partition(0, _graph(v, adj, gids, eo))
+    got = ctx.beam_search_sharded_emulated(3, q, dvs.SearchParams(I, w, k, E, accum="f32"))
+    _assert_same(got, want, True, (gid_order, "bulk sharded"))
+
+
 def test_global_hash_path_matches_oracle(ctx, oracle):
     # bound = min(n, E + I*w*dg) > 16384 -> the visited hash lives in global memory
     n, dim = 20000, 8
@@ -279,8 +305,9 @@ def test_load_index_format_errors(ctx, tmp_path):
 
 # ---- node-sharded search (ranks emulated in one launch) ------------------------
 
+@pytest.mark.parametrize("exchange", ["bulk", "fused"])
 @pytest.mark.parametrize("nranks", [1, 2, 3, 4, 8])
-def test_sharded_emulated_matches_unsharded(ctx, oracle, nranks):
+def test_sharded_emulated_matches_unsharded(ctx, oracle, nranks, exchange):
     n, dim = 3000, 32
     v = sift_like(n, dim, 6, 91)
     adj = oracle.build_graph(v, 32)
@@ -292,8 +319,33 @@ def test_sharded_emulated_matches_unsharded(ctx, oracle, nranks):
     ctx.reset()
     ctx._single_key = None
     ctx.load_partition(0, _graph(v, adj, gids, eo))
-    got = ctx.beam_search_sharded_emulated(nranks, q, p)
-    _assert_same(got, want, True, f"sharded R={nranks}")
+    ctx.set_shard_exchange(exchange)
+    try:
+        got = ctx.beam_search_sharded_emulated(nranks, q, p)
+    finally:
+        ctx.set_shard_exchange("bulk")
+    _assert_same(got, want, True, f"sharded {exchange} R={nranks}")
+
+
+def test_sharded_bulk_waves_and_shapes(ctx, oracle, monkeypatch):
+    """Bulk exchange split into many small waves (DVSG_XG_WAVE), odd dim,
+    ragged rank split, tiny partition (entry_count > n), IP metric, f64."""
+    monkeypatch.setenv("DVSG_XG_WAVE", "7")
+    for (n, dim, nq, R, w, k, E, metric, accum) in [(2500, 37, 61, 3, 16, 10, 16, "l2", "f32"),
+                                                      (40, 8, 23, 4, 8, 20, 64, "l2", "f64"),
+                                                      (1800, 24, 50, 2, 32, 5, 32, "ip", "f32")]:
+        v = sift_like(n, dim, 6, 301 + n)
+        adj = oracle.build_graph(v, 16)
+        eo = oracle.compute_entry_order(v)
+        q = sift_like(nq, dim, 6, 302 + n)
+        gids = (7 + 3 * np.arange(n)).astype(np.uint32)
+        p = dvs.SearchParams(5, w, k, E, metric=metric, accum=accum)
+        ctx.reset()
+        ctx._single_key = None
+        ctx.load_partition(0, _graph(v, adj, gids, eo))
+        want = ctx.beam_search(0, q, p)
+        got = ctx.beam_search_sharded_emulated(R, q, p)
+        _assert_same(got, want, True, ("bulk waves", n, dim, R, metric))
 
 
 def test_sharded_emulated_golden(ctx, golden):
