@@ -65,8 +65,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cache", default="/tmp/dvsg_bench_cache")
     ap.add_argument("--mode", choices=["auto", "replica", "sharded"], default="auto",
-                    help="N>1 layout: full index per GPU, or node-sharded vectors with the fused "
-                         "NVLink frontier exchange (auto = sharded when N>1)")
+                    help="N>1 layout: full index per GPU, or node-sharded vectors with an NVLink "
+                         "frontier exchange (auto = replica headline, sharded measured beside it)")
+    ap.add_argument("--exchange", choices=["bulk", "fused"], default="bulk",
+                    help="sharded-mode exchange: bulk-synchronous phases (xchg_kernel.cu) or "
+                         "per-CTA round trips (shard_kernel.cu)")
     return ap.parse_args()
 
 
@@ -273,6 +276,7 @@ def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, i
     from paper_2512_02278_b200.dist import prepare_step, setup_sharded
     g0 = index.graphs[0]
     ctx = dvs.Context(local)
+    ctx.set_shard_exchange(args.exchange)
     setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
     nq, dim, k = args.nq, args.dim, args.k
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
@@ -310,8 +314,9 @@ def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, i
     ms = float(t[0])
     return {"value": nq * world * args.steps / (ms / 1e3), "unit": "queries/s",
             "ms_per_step": ms / args.steps,
-            "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; "
-                      "fused NVLink peer-store frontier exchange (shard_kernel.cu)",
+            "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; " + (
+                "bulk-synchronous NVLink peer-store frontier exchange (xchg_kernel.cu)" if args.exchange == "bulk"
+                else "fused NVLink peer-store frontier exchange (shard_kernel.cu)"),
             "ids_identical_to_replica_all_ranks": bool(same[0])}
 
 
@@ -350,6 +355,7 @@ def main():
     g0 = index.graphs[0]
     if sharded:
         from paper_2512_02278_b200.dist import prepare_step, setup_sharded
+        ctx.set_shard_exchange(args.exchange)
         setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
     else:
         ctx.load_index(index)

@@ -137,12 +137,14 @@ struct XgArgs {
   unsigned long long* work_counter;
   unsigned long long* stats;  // [0] units, [1] visited, [2] expanded
   int* err;
-  int expand_ctas, score_ctas;  // > 0: CTAs per SM of each kernel (room for the other lane)
 };
 
 size_t xg_expand_smem_bytes(int cap, int chp, int beam, int maxraw);
-cudaError_t launch_xg_expand(const XgArgs& a, int num_sms, cudaStream_t stream);
-cudaError_t launch_xg_score(const XgArgs& a, int metric, int accum, int num_sms, cudaStream_t stream);
+// One phase step (xg_step): expand items of lane ea (do_e) and score items of
+// lane sa (do_s), claimed interleaved from *counter (zeroed by the caller).
+cudaError_t launch_xg_step(const XgArgs& ea, const XgArgs& sa, int do_e, int do_s,
+                           unsigned long long* counter, int metric, int accum, int num_sms,
+                           cudaStream_t stream);
 // Peer-flag barrier over all ranks (one thread); sets bit 3 of *err after a 20 s timeout.
 cudaError_t launch_xg_barrier(const XgView* views, int nranks, int me, unsigned epoch, int* err,
                               cudaStream_t stream);

@@ -178,12 +178,9 @@ struct dvsg_ctx {
     DevBuf<unsigned long long> counters;
     DevBuf<int> err;
     unsigned epoch[4] = {0, 0, 0, 0};
-    bool kind_recorded[2][4] = {};
     bool issued = false;
   } xg;
-  cudaStream_t xg_streams[4] = {};   // lanes 1.. of the bulk exchange (lane 0: stream)
-  cudaEvent_t xg_ev[4] = {};
-  cudaEvent_t xg_kind_ev[2][4] = {};
+
   int shard_exchange = -1;                     // 0 bulk (default), 1 fused; -1: env DVSG_SHARD_EXCHANGE
   DevBuf<unsigned char> emu_arena;             // emulation: all virtual ranks' arenas
   DevBuf<dvsg::ShardView> d_views;
@@ -655,7 +652,6 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
   x.expd.reserve(st_n, c->stream);
   x.hash.reserve(st_n * k.hsize, c->stream);
   x.meta.reserve(st_n * (uint64_t)R, c->stream);
-  x.counters.reserve((size_t)L * ((size_t)p->iterations + 2), c->stream);
   x.err.reserve(1, c->stream);
   cuda_check(cudaMemsetAsync(x.err.p, 0, sizeof(int), c->stream), "err reset");
 
@@ -708,10 +704,7 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
   base.out_stride = emulate ? upr : 0;
   base.stats = ka.stats;
   base.err = x.err.p;
-  base.expand_ctas = (int)env_u64("DVSG_XG_EXPAND_CTAS", L > 1 ? 2 : 0);
-  base.score_ctas = (int)env_u64("DVSG_XG_SCORE_CTAS", L > 1 ? 2 : 0);
   dvsg::XgArgs la[kXgLanes];
-  cudaStream_t ls[kXgLanes];
   for (int l = 0; l < L; ++l) {
     la[l] = base;
     la[l].views = x.d_views.p + (size_t)l * R;
@@ -722,34 +715,19 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
     la[l].expd = x.expd.p + so;
     la[l].hash = x.hash.p + so * k.hsize;
     la[l].meta = x.meta.p + so * (uint64_t)R;
-    ls[l] = l == 0 ? c->stream : c->xg_streams[l];
   }
-  // lane streams start after everything queued so far on the compute stream
-  cuda_check(cudaEventRecord(c->xg_ev[0], c->stream), "event");
-  for (int l = 1; l < L; ++l) cuda_check(cudaStreamWaitEvent(ls[l], c->xg_ev[0], 0), "wait");
-
   auto barrier = [&](int l) {
     if (emulate) return;  // stream order is the barrier
     x.epoch[l] += 1;
-    cuda_check(dvsg::launch_xg_barrier(la[l].views, R, me, x.epoch[l], x.err.p, ls[l]), "xg barrier");
+    cuda_check(dvsg::launch_xg_barrier(la[l].views, R, me, x.epoch[l], x.err.p, c->stream), "xg barrier");
     c->launches += 1;
   };
-  // half-phase offset between lanes: lane l's kernel of a kind waits for
-  // lane l-1's kernel of the same kind (and lane 0 for the last lane's)
-  const bool stagger = L > 1 && env_u64("DVSG_XG_STAGGER", 1) != 0;
-  auto after = [&](int l, int kind) {  // kind 0 expand, 1 score
-    if (!stagger) return;
-    const int prev = (l + L - 1) % L;
-    cudaEvent_t e = c->xg_kind_ev[kind][prev];
-    if (x.kind_recorded[kind][prev]) cuda_check(cudaStreamWaitEvent(ls[l], e, 0), "wait");
-  };
-  auto done = [&](int l, int kind) {
-    if (!stagger) return;
-    cuda_check(cudaEventRecord(c->xg_kind_ev[kind][l], ls[l]), "event");
-    x.kind_recorded[kind][l] = true;
-  };
-  for (int l = 0; l < kXgLanes; ++l) x.kind_recorded[0][l] = x.kind_recorded[1][l] = false;
-
+  // Per lane the ops are E0 S0 E1 S1 ... E_I S_I E_{I+1} (E_{I+1}: finalize).
+  // Launch t runs lane 0's op t and lane 1's op t-1: one expand and one score
+  // per launch, co-resident in one xg_step grid.
+  const int nops = 2 * (p->iterations + 1) + 1;
+  const int nlaunch = nops + L - 1;
+  x.counters.reserve(2 * (size_t)nlaunch, c->stream);
   if (c->timing) cudaEventRecord(c->ev[0], c->stream);
   for (uint64_t w0 = 0; w0 < nwaves; w0 += (uint64_t)L) {
     for (int l = 0; l < L; ++l) {
@@ -767,42 +745,42 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
         for (int r = 0; r < (emulate ? 1 : R); ++r) {
           float* dst = views[(size_t)l * R + r].qall + (uint64_t)o * wcap * (uint64_t)c->dpad;
           cuda_check(cudaMemcpy2DAsync(dst, (size_t)c->dpad * 4, src, (size_t)dim * 4, (size_t)dim * 4,
-                                       a.wave_n[rr], cudaMemcpyDefault, ls[l]), "push queries");
+                                       a.wave_n[rr], cudaMemcpyDefault, c->stream), "push queries");
         }
       }
       a.out_ids = d_ids + off * (uint64_t)p->k;
       a.out_dists = d_dists + off * (uint64_t)p->k;
       a.out_count = d_count + off;
       a.out_visited = d_visited + off;
-      unsigned long long* ctr = x.counters.p + (size_t)l * ((size_t)p->iterations + 2);
-      cuda_check(cudaMemsetAsync(ctr, 0, ((size_t)p->iterations + 2) * sizeof(unsigned long long), ls[l]), "counters");
       barrier(l);  // every owner holds this wave's queries
     }
-    for (int ph = 0; ph <= p->iterations + 1; ++ph) {
+    cuda_check(cudaMemsetAsync(x.counters.p, 0, 2 * (size_t)nlaunch * sizeof(unsigned long long), c->stream), "counters");
+    for (int t = 0; t < nlaunch; ++t) {
+      int le = -1, ls = -1;  // lanes doing an expand / a score op in this launch
       for (int l = 0; l < L; ++l) {
-        auto& a = la[l];
-        a.phase = ph;
-        a.work_counter = x.counters.p + (size_t)l * ((size_t)p->iterations + 2) + ph;
-        after(l, 0);
-        cuda_check(dvsg::launch_xg_expand(a, c->num_sms, ls[l]), "xg expand");
-        done(l, 0);
-        c->launches += 1;
-        if (ph > p->iterations) continue;  // finalize pass
-        barrier(l);  // requests delivered
-        after(l, 1);
-        cuda_check(dvsg::launch_xg_score(a, p->metric, p->accum, c->num_sms, ls[l]), "xg score");
-        done(l, 1);
-        c->launches += 1;
-        // this phase's inbox cursors are free again (next used two barriers later)
-        for (int rr = 0; rr < rank_n; ++rr)
-          cuda_check(cudaMemsetAsync(views[(size_t)l * R + me + rr].cursor + (ph & 1) * R, 0, (size_t)R * 4, ls[l]), "cursor reset");
-        barrier(l);  // replies delivered
+        const int op = t - l;
+        if (op < 0 || op >= nops) continue;
+        if (op & 1) {
+          ls = l;
+          la[l].phase = op >> 1;
+        } else {
+          le = l;
+          la[l].phase = op >> 1;
+        }
       }
+      const dvsg::XgArgs& ea = la[le >= 0 ? le : ls];
+      const dvsg::XgArgs& sa = la[ls >= 0 ? ls : le];
+      cuda_check(dvsg::launch_xg_step(ea, sa, le >= 0, ls >= 0, x.counters.p + 2 * t, p->metric, p->accum,
+                                      c->num_sms, c->stream), "xg step");
+      c->launches += 1;
+      if (ls >= 0)  // that phase's inbox cursors are free again (next used two barriers later)
+        for (int rr = 0; rr < rank_n; ++rr)
+          cuda_check(cudaMemsetAsync(views[(size_t)ls * R + me + rr].cursor + (la[ls].phase & 1) * R, 0,
+                                     (size_t)R * 4, c->stream), "cursor reset");
+      // requests (after an expand) / replies (after a score) delivered
+      if (le >= 0 && la[le].phase <= p->iterations) barrier(le);
+      if (ls >= 0) barrier(ls);
     }
-  }
-  for (int l = 1; l < L; ++l) {
-    cuda_check(cudaEventRecord(c->xg_ev[l], ls[l]), "event");
-    cuda_check(cudaStreamWaitEvent(c->stream, c->xg_ev[l], 0), "join");
   }
   if (c->timing) {
     cudaEventRecord(c->ev[1], c->stream);
@@ -999,10 +977,7 @@ dvsg_status dvsg_create(int device, dvsg_ctx** out) {
     c->smem_optin = prop.sharedMemPerBlockOptin;
     cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     cuda_check(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking), "stream");
-    for (int l = 1; l < 4; ++l) cuda_check(cudaStreamCreateWithFlags(&c->xg_streams[l], cudaStreamNonBlocking), "stream");
-    for (auto& e : c->xg_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    for (auto& row : c->xg_kind_ev)
-      for (auto& e : row) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
     for (auto& e : c->mb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     *out = c.release();
@@ -1021,10 +996,7 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     for (auto& e : c->mb_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm);
-    for (int l = 1; l < 4; ++l) cudaStreamDestroy(c->xg_streams[l]);
-    for (auto& e : c->xg_ev) cudaEventDestroy(e);
-    for (auto& row : c->xg_kind_ev)
-      for (auto& e : row) cudaEventDestroy(e);
+
     delete c;
   });
 }

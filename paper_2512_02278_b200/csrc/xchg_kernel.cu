@@ -76,14 +76,11 @@ struct XgShared {
   uint2 meta[kXgMaxRanks];
 };
 
-#ifndef DVSG_XG_EXPAND_MINB
-#define DVSG_XG_EXPAND_MINB 4
-#endif
-__global__ void __launch_bounds__(kThreads, DVSG_XG_EXPAND_MINB) xg_expand(const XgArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ BlockState st;
-  __shared__ XgShared xs;
-
+// One query of the origin's wave: merge the previous phase's replies, then
+// (phases <= iters) pick the frontier, dedup, push the requests, or
+// (phase iters + 1) write the result.  Block-uniform call.
+__device__ __forceinline__ void expand_unit(const XgArgs& a, const int rr, const uint32_t j,
+                                            unsigned char* smem, BlockState& st, XgShared& xs) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int R = a.nranks;
   uint64_t* pool = reinterpret_cast<uint64_t*>(smem);
@@ -99,27 +96,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_XG_EXPAND_MINB) xg_expand(const
   const bool entry_phase = a.phase == 0;
   const bool final_phase = a.phase > a.iters;
   const int slot = a.phase & 1;
-
-  for (;;) {
-    if (tid == 0) {
-      uint64_t t = atomicAdd(a.work_counter, 1ull);
-      uint64_t u = ~0ull;
-      if (*a.err == 0) {
-        for (int r = 0; r < a.rank_n; ++r) {
-          if (t < a.wave_n[r]) {
-            u = ((uint64_t)r << 32) | t;
-            break;
-          }
-          t -= a.wave_n[r];
-        }
-      }
-      st.unit = u;
-    }
-    __syncthreads();
-    const uint64_t unit = st.unit;
-    if (unit == ~0ull) break;
-    const int rr = (int)(unit >> 32);
-    const uint32_t j = (uint32_t)unit;
+  {
     const int me = a.rank_lo + rr;
     const uint64_t qs = (uint64_t)rr * a.wcap + j;
     uint32_t* table = a.hash + qs * (uint64_t)a.hsize;
@@ -235,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_XG_EXPAND_MINB) xg_expand(const
         }
       }
       __syncthreads();
-      continue;
+      return;
     }
 
     // ---- raw candidates: entry nodes, or the frontier's adjacency rows
@@ -387,11 +364,30 @@ __global__ void __launch_bounds__(kThreads, DVSG_XG_EXPAND_MINB) xg_expand(const
     }
     __syncthreads();
   }
-  __threadfence_system();  // release this CTA's peer stores before the barrier kernel
 }
 
-// Owner side: score every request in this rank's inbox (all origins), push
-// the keys back.  Warp per 32 consecutive requests of one origin.
+// Owner side, per phase: per-CTA table of the inbox segments (acting rank x
+// origin) in 32-request warp blocks.
+struct ScoreTable {
+  uint64_t pref[kXgMaxRanks * kXgMaxRanks + 1];
+  uint32_t cnt[kXgMaxRanks * kXgMaxRanks];
+  int nseg;
+};
+
+__device__ __forceinline__ void score_table(const XgArgs& a, ScoreTable& t) {
+  if (threadIdx.x == 0) {
+    const int R = a.nranks, slot = a.phase & 1;
+    t.nseg = a.rank_n * R;
+    t.pref[0] = 0;
+    for (int s = 0; s < t.nseg; ++s) {
+      const int r = a.rank_lo + s / R, o = s % R;
+      const uint32_t c = *a.err ? 0u : __ldcg(a.views[r].cursor + slot * R + o);
+      t.cnt[s] = c;
+      t.pref[s + 1] = t.pref[s] + (c + 31u) / 32u;
+    }
+  }
+}
+
 // lane's slice of a dpad-strided query row (dims >= dim read as 0)
 template <int VPL, bool FULL>
 __device__ __forceinline__ void load_query(float4 (&q)[VPL], const float* qp, int lane, int dim) {
@@ -409,37 +405,23 @@ __device__ __forceinline__ void load_query(float4 (&q)[VPL], const float* qp, in
   }
 }
 
+// Score warp block b (32 consecutive requests of one origin) and push the
+// keys back into the origin's reply range.  Warp-collective.
 template <int VPL, typename ACC, int METRIC, bool FULL>
-#ifndef DVSG_XG_SCORE_MINB
-#define DVSG_XG_SCORE_MINB 4  // fp32 path: 64 registers (fp64 partials keep 3 CTAs/SM)
-#endif
-__global__ void __launch_bounds__(kThreads, sizeof(ACC) == 8 ? 3 : DVSG_XG_SCORE_MINB) xg_score(const XgArgs a) {
+__device__ __forceinline__ void score_warp_block(const XgArgs& a, const ScoreTable& t, uint64_t b,
+                                                 uint64_t* wq, uint64_t* wk) {
   constexpr int U = VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL);
   constexpr int LU = ilog2(U);
-  __shared__ uint64_t pref[kXgMaxRanks * kXgMaxRanks + 1];
-  __shared__ uint32_t scnt[kXgMaxRanks * kXgMaxRanks];
-  __shared__ __align__(16) uint64_t wreq[kThreads];
-  __shared__ uint64_t wkey[kThreads];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int R = a.nranks, nseg = a.rank_n * R, slot = a.phase & 1;
-  if (tid == 0) {
-    pref[0] = 0;
-    for (int s = 0; s < nseg; ++s) {
-      const int r = a.rank_lo + s / R, o = s % R;
-      const uint32_t c = *a.err ? 0u : __ldcg(a.views[r].cursor + slot * R + o);
-      scnt[s] = c;
-      pref[s + 1] = pref[s] + (c + 31u) / 32u;
-    }
-  }
-  __syncthreads();
-  const uint64_t total = pref[nseg];
-  int s = 0, cur_s = -1;
+  const int lane = threadIdx.x & 31;
+  const int R = a.nranks;
+  int s = 0;
+  while (b >= t.pref[s + 1]) ++s;
+  const uint32_t* scnt = t.cnt;
   uint32_t cur_q = kEmpty;
   float4 q[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) q[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (uint64_t b = (uint64_t)blockIdx.x * kWarps + warp; b < total; b += (uint64_t)gridDim.x * kWarps) {
-    while (b >= pref[s + 1]) ++s;
+  const uint64_t* pref = t.pref;
     const int r = a.rank_lo + s / R, o = s % R;
     const uint32_t e0 = (uint32_t)(b - pref[s]) * 32u;
     const int ne = (int)min(32u, scnt[s] - e0);
@@ -448,15 +430,9 @@ __global__ void __launch_bounds__(kThreads, sizeof(ACC) == 8 ? 3 : DVSG_XG_SCORE
     const uint32_t lo = (uint32_t)vr.lo;
     const float* qbase = vr.qall + (uint64_t)o * a.wcap * (uint64_t)a.dpad;
     // stage the 32 requests in smem; rounds read them back as broadcasts
-    uint64_t* wq = wreq + warp * 32;
-    uint64_t* wk = wkey + warp * 32;
     __syncwarp();  // previous block's readers are done with wq / wk
     wq[lane] = lane < ne ? __ldcg(vr.inbox + (uint64_t)o * a.rstride + e0 + lane) : (uint64_t)lo;
     __syncwarp();
-    if (s != cur_s) {
-      cur_s = s;
-      cur_q = kEmpty;
-    }
 #pragma unroll 1
     for (int round = 0; round < 32 / U; ++round) {
       if (round * U >= ne) break;  // warp-uniform
@@ -528,8 +504,64 @@ __global__ void __launch_bounds__(kThreads, sizeof(ACC) == 8 ? 3 : DVSG_XG_SCORE
     }
     __syncwarp();
     if (lane < ne) a.views[o].reply[(uint64_t)r * a.rstride + e0 + lane] = wk[lane];
+}
+
+#ifndef DVSG_XG_MINB
+#define DVSG_XG_MINB 4  // fp32: 64 registers (fp64 partials keep 3 CTAs/SM)
+#endif
+// One phase step: expand items of lane `ea` (do_e) and score items of lane
+// `sa` (do_s) from one work counter, interleaved, so origin-side work
+// (latency / issue bound) and owner-side gathers (HBM bound) share the SMs.
+template <int VPL, typename ACC, int METRIC, bool FULL>
+__global__ void __launch_bounds__(kThreads, sizeof(ACC) == 8 ? 3 : DVSG_XG_MINB)
+xg_step(const XgArgs ea, const XgArgs sa, int do_e, int do_s, unsigned long long* counter) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ BlockState st;
+  __shared__ XgShared xs;
+  __shared__ ScoreTable tab;
+  __shared__ __align__(16) uint64_t wreq[kThreads];
+  __shared__ uint64_t wkey[kThreads];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (do_s) score_table(sa, tab);
+  __syncthreads();
+  uint64_t nE = 0;
+  if (do_e)
+    for (int r = 0; r < ea.rank_n; ++r) nE += ea.wave_n[r];
+  const uint64_t nwb = do_s ? tab.pref[tab.nseg] : 0;  // score warp blocks
+  // CTAs alternate a preferred kind (so every SM runs both), then help with
+  // the other kind; expand items are per CTA, score blocks per warp.
+  const bool prefer_s = do_s && (!do_e || (blockIdx.x & 1));
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool s_mode = (pass == 0) == prefer_s;
+    if (s_mode) {
+      if (!do_s) continue;
+      const int lane = tid & 31;
+      for (;;) {
+        uint64_t b = 0;
+        if (lane == 0) b = *sa.err ? ~0ull : atomicAdd(counter + 1, 1ull);
+        b = __shfl_sync(0xFFFFFFFFu, b, 0);
+        if (b >= nwb) break;
+        score_warp_block<VPL, ACC, METRIC, FULL>(sa, tab, b, wreq + warp * 32, wkey + warp * 32);
+      }
+      __syncthreads();  // every warp is done before the CTA claims expand items
+    } else {
+      if (!do_e) continue;
+      for (;;) {
+        if (tid == 0) {
+          const uint64_t t = *ea.err ? ~0ull : atomicAdd(counter, 1ull);
+          st.unit = t < nE ? t : ~0ull;
+        }
+        __syncthreads();
+        uint64_t u = st.unit;
+        __syncthreads();  // st is reused by expand_unit
+        if (u == ~0ull) break;
+        int rr = 0;
+        while (u >= ea.wave_n[rr]) u -= ea.wave_n[rr++];
+        expand_unit(ea, rr, (uint32_t)u, smem, st, xs);
+      }
+    }
   }
-  __threadfence_system();  // release the peer stores before the barrier kernel
+  __threadfence_system();  // release this CTA's peer stores before the barrier kernel
 }
 
 __global__ void xg_barrier(const XgView* views, int nranks, int me, unsigned epoch, int* err) {
@@ -551,30 +583,34 @@ __global__ void xg_barrier(const XgView* views, int nranks, int me, unsigned epo
 }
 
 template <int VPL, typename ACC, int METRIC, bool FULL>
-cudaError_t launch_score_t(const XgArgs& a, int num_sms, cudaStream_t stream) {
-  auto kern = xg_score<VPL, ACC, METRIC, FULL>;
+cudaError_t launch_step_t(const XgArgs& ea, const XgArgs& sa, int do_e, int do_s,
+                          unsigned long long* counter, int num_sms, cudaStream_t stream) {
+  auto kern = xg_step<VPL, ACC, METRIC, FULL>;
+  const size_t smem = xg_expand_smem_bytes(ea.cap, ea.chp, ea.beam, (int)ea.maxraw);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  if (a.score_ctas > 0 && a.score_ctas < per_sm) per_sm = a.score_ctas;
-  kern<<<(unsigned)(per_sm * num_sms), kThreads, 0, stream>>>(a);
+  kern<<<(unsigned)(per_sm * num_sms), kThreads, smem, stream>>>(ea, sa, do_e, do_s, counter);
   return cudaGetLastError();
 }
 
 template <int VPL>
-cudaError_t launch_score_v(const XgArgs& a, int metric, int accum, int num_sms, cudaStream_t s) {
-  const bool full = a.dpad == 128 * VPL;
+cudaError_t launch_step_v(const XgArgs& ea, const XgArgs& sa, int do_e, int do_s, unsigned long long* ctr,
+                          int metric, int accum, int num_sms, cudaStream_t s) {
+  const bool full = ea.dpad == 128 * VPL;
   if (accum == 0) {
-    if (metric == 0) return full ? launch_score_t<VPL, double, 0, true>(a, num_sms, s)
-                                 : launch_score_t<VPL, double, 0, false>(a, num_sms, s);
-    return full ? launch_score_t<VPL, double, 1, true>(a, num_sms, s)
-                : launch_score_t<VPL, double, 1, false>(a, num_sms, s);
+    if (metric == 0) return full ? launch_step_t<VPL, double, 0, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
+                                 : launch_step_t<VPL, double, 0, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
+    return full ? launch_step_t<VPL, double, 1, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
+                : launch_step_t<VPL, double, 1, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
   }
-  if (metric == 0) return full ? launch_score_t<VPL, float, 0, true>(a, num_sms, s)
-                               : launch_score_t<VPL, float, 0, false>(a, num_sms, s);
-  return full ? launch_score_t<VPL, float, 1, true>(a, num_sms, s)
-              : launch_score_t<VPL, float, 1, false>(a, num_sms, s);
+  if (metric == 0) return full ? launch_step_t<VPL, float, 0, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
+                               : launch_step_t<VPL, float, 0, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
+  return full ? launch_step_t<VPL, float, 1, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
+              : launch_step_t<VPL, float, 1, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
 }
 
 }  // namespace
@@ -584,32 +620,16 @@ size_t xg_expand_smem_bytes(int cap, int chp, int beam, int maxraw) {
          sizeof(uint32_t) * (2 * (size_t)maxraw + (size_t)((beam + 3) & ~3));
 }
 
-cudaError_t launch_xg_expand(const XgArgs& a, int num_sms, cudaStream_t stream) {
-  const size_t smem = xg_expand_smem_bytes(a.cap, a.chp, a.beam, (int)a.maxraw);
-  cudaError_t e = cudaFuncSetAttribute(xg_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, xg_expand, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  if (a.expand_ctas > 0 && a.expand_ctas < per_sm) per_sm = a.expand_ctas;
-  uint64_t units = 0;
-  for (int r = 0; r < a.rank_n; ++r) units += a.wave_n[r];
-  uint64_t grid = (uint64_t)per_sm * (uint64_t)num_sms;
-  if (grid > units) grid = units;
-  if (grid < 1) grid = 1;
-  xg_expand<<<(unsigned)grid, kThreads, smem, stream>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_xg_score(const XgArgs& a, int metric, int accum, int num_sms, cudaStream_t s) {
-  switch ((a.dpad + 127) / 128) {
-    case 1: return launch_score_v<1>(a, metric, accum, num_sms, s);
-    case 2: return launch_score_v<2>(a, metric, accum, num_sms, s);
+cudaError_t launch_xg_step(const XgArgs& ea, const XgArgs& sa, int do_e, int do_s,
+                           unsigned long long* counter, int metric, int accum, int num_sms,
+                           cudaStream_t s) {
+  switch ((ea.dpad + 127) / 128) {
+    case 1: return launch_step_v<1>(ea, sa, do_e, do_s, counter, metric, accum, num_sms, s);
+    case 2: return launch_step_v<2>(ea, sa, do_e, do_s, counter, metric, accum, num_sms, s);
     case 3:
-    case 4: return launch_score_v<4>(a, metric, accum, num_sms, s);
+    case 4: return launch_step_v<4>(ea, sa, do_e, do_s, counter, metric, accum, num_sms, s);
     case 5:
-    case 6: return launch_score_v<6>(a, metric, accum, num_sms, s);
+    case 6: return launch_step_v<6>(ea, sa, do_e, do_s, counter, metric, accum, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -16,5 +16,5 @@ for r in rows:
 xs = [o for o in out if "xg_" in o[0]]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 last = xs[-n:]
-print("expand %.2f ms  score %.2f ms" % (sum(t for k, t in last if "expand" in k), sum(t for k, t in last if "score" in k)))
-print(" ".join("%s%.2f" % ("E" if "expand" in k else "S", t) for k, t in last))
+print("total %.2f ms over the last %d xg launches" % (sum(t for k, t in last), len(last)))
+print(" ".join("%.2f" % t for k, t in last))
