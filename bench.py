@@ -67,9 +67,12 @@ def parse():
     ap.add_argument("--mode", choices=["auto", "replica", "sharded"], default="auto",
                     help="N>1 layout: full index per GPU, or node-sharded vectors with an NVLink "
                          "frontier exchange (auto = replica headline, sharded measured beside it)")
-    ap.add_argument("--exchange", choices=["bulk", "fused"], default="bulk",
+    ap.add_argument("--no-nccl-baseline", action="store_true",
+                    help="skip the NCCL-exchange baseline measured beside the sharded mode at N>1")
+    ap.add_argument("--exchange", choices=["bulk", "fused", "nccl"], default="bulk",
                     help="sharded-mode exchange: bulk-synchronous phases (xchg_kernel.cu) or "
-                         "per-CTA round trips (shard_kernel.cu)")
+                         "per-CTA round trips (shard_kernel.cu), or the bulk protocol over "
+                         "host-driven NCCL send/recv (the measured baseline)")
     return ap.parse_args()
 
 
@@ -261,9 +264,9 @@ def workload_config(args, world, rec):
         "recall_at_10": None if rec is None else round(rec, 4),
         "l2": "256 MiB buffer written before every timed step",
         "parallelism": (f"node-sharded x{world}: vectors split by id range, adjacency replicated, "
-                        "fused NVLink peer-store frontier exchange" if getattr(args, "_sharded", False)
+                        f"{args.exchange} NVLink peer-store frontier exchange" if getattr(args, "_sharded", False)
                         else (f"replicas x{world}" if world > 1 else "single GPU")),
-        "step": ("K1 sharded search (ids + dists)" if getattr(args, "_sharded", False)
+        "step": ("node-sharded search (ids + dists)" if getattr(args, "_sharded", False)
                  else "run_pipeline: assign + route + K1 + combine + hit vectors"),
     }
 
@@ -272,12 +275,15 @@ def workload_config(args, world, rec):
 def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, index, p, ids_ref,
                     cnt_ref, flush, dev):
     """K timed steps of the node-sharded search (vectors split across the N
-    GPUs, fused NVLink frontier exchange); ids must equal the replica run's."""
+    GPUs, NVLink frontier exchange, --exchange); ids must equal the replica run's."""
     from paper_2512_02278_b200.dist import prepare_step, setup_sharded
     g0 = index.graphs[0]
     ctx = dvs.Context(local)
     ctx.set_shard_exchange(args.exchange)
     setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
+    if args.exchange == "nccl":
+        from paper_2512_02278_b200.dist import connect_nccl
+        connect_nccl(ctx, rank)
     nq, dim, k = args.nq, args.dim, args.k
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     d_q = torch.from_numpy(queries).to(dev)
@@ -316,7 +322,9 @@ def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, i
             "ms_per_step": ms / args.steps,
             "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; " + (
                 "bulk-synchronous NVLink peer-store frontier exchange (xchg_kernel.cu)" if args.exchange == "bulk"
+                else "bulk protocol, host-driven ncclSend/ncclRecv exchange (baseline)" if args.exchange == "nccl"
                 else "fused NVLink peer-store frontier exchange (shard_kernel.cu)"),
+            "exchange": args.exchange,
             "ids_identical_to_replica_all_ranks": bool(same[0])}
 
 
@@ -357,6 +365,9 @@ def main():
         from paper_2512_02278_b200.dist import prepare_step, setup_sharded
         ctx.set_shard_exchange(args.exchange)
         setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
+        if args.exchange == "nccl":
+            from paper_2512_02278_b200.dist import connect_nccl
+            connect_nccl(ctx, rank)
     else:
         ctx.load_index(index)
     p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
@@ -512,6 +523,16 @@ def main():
     if world > 1 and not sharded and args.mode == "auto":
         sharded_side = measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries,
                                        index, p, ids_h, cnt_h, flush, dev)
+        if args.exchange != "nccl" and not args.no_nccl_baseline:
+            # the same protocol over host-driven NCCL send/recv: the measured baseline
+            ex = args.exchange
+            args.exchange = "nccl"
+            try:
+                sharded_side["nccl_baseline"] = measure_sharded(
+                    args, dvs, torch, dist, local, rank, world, data, queries, index, p, ids_h, cnt_h,
+                    flush, dev)
+            finally:
+                args.exchange = ex
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------------
     cpu = None
@@ -555,7 +576,10 @@ def main():
         "data": "synthetic", "config": workload_config(args, world, rec),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "dvsg::search_kernel (K1)",
+                     "kernel": ("dvsg::search_kernel (K1)" if not getattr(args, "_sharded", False) else
+                                ("dvsg::xg_step (bulk exchange)" if args.exchange == "bulk"
+                                 else "dvsg::xg_step (bulk protocol, NCCL exchange)" if args.exchange == "nccl"
+                                 else "dvsg::search_sharded_kernel (fused exchange)")),
                      "k1_ms_per_step": k1_max_ms / args.steps,
                      "alg_bytes_per_step": alg_bytes / args.steps,
                      "visited_per_query": vis_tot / max(units_tot, 1),

@@ -168,12 +168,21 @@ dvsg_status dvsg_search_sharded_device(dvsg_ctx *ctx, const float *d_queries, ui
  *      new candidates into the owners' inboxes, a peer-flag barrier, xg_score
  *      scores them and pushes the keys back, a barrier (xchg_kernel.cu);
  *   1  fused: one persistent kernel, per-CTA request/reply round trips
- *      (shard_kernel.cu).
- * Default from the environment (DVSG_SHARD_EXCHANGE=fused), else 0.  With the
+ *      (shard_kernel.cu);
+ *   2  nccl: see below.
+ * Default from the environment (DVSG_SHARD_EXCHANGE=fused|nccl), else 0.  With the
  * bulk exchange, dvsg_search_sharded_device is collective: every rank must
  * call it with the same nq and params; dvsg_synchronize reports a rank that
  * never reached a barrier (DVSG_EINTERNAL after 20 s). */
 dvsg_status dvsg_set_shard_exchange(dvsg_ctx *ctx, int mode);
+/* Mode 2 -- the NCCL baseline of the bulk exchange (north_star: "an NCCL
+ * all-to-all variant kept only as the measured baseline"): the same
+ * xg_step kernels over local send/receive slabs, with host-driven
+ * ncclSend/ncclRecv of the requests and replies after each half-phase (their
+ * sizes go through the host, two stream syncs per phase).  libnccl.so.2 is
+ * loaded at run time.  Rank 0 creates the id, every rank connects with it. */
+dvsg_status dvsg_nccl_unique_id(dvsg_ctx *ctx, void *id_out128);
+dvsg_status dvsg_nccl_connect(dvsg_ctx *ctx, const void *id128);
 
 /* ---- routing and merge -------------------------------------------------- */
 

@@ -78,6 +78,8 @@ _SIGS = {
     "dvsg_brute_force_topk": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_uint64, c_int,
                                       c_void_p, c_void_p]),
     "dvsg_set_shard_exchange": (c_int, [c_void_p, c_int]),
+    "dvsg_nccl_unique_id": (c_int, [c_void_p, c_void_p]),
+    "dvsg_nccl_connect": (c_int, [c_void_p, c_void_p]),
     "dvsg_set_timing": (c_int, [c_void_p, c_int]),
     "dvsg_last_timings": (c_int, [c_void_p, P_f32, P_f32, P_f32, P_f32]),
     "dvsg_kernel_launches": (c_uint64, [c_void_p]),

@@ -285,9 +285,20 @@ class Context:
         check(lib.dvsg_shard_connect(self._h, buf))
 
     def set_shard_exchange(self, mode: str) -> None:
-        """'bulk' (bulk-synchronous phases, xchg_kernel.cu; default) or 'fused'
-        (per-CTA round trips, shard_kernel.cu); both exact."""
-        check(lib.dvsg_set_shard_exchange(self._h, {"bulk": 0, "fused": 1}[mode]))
+        """'bulk' (bulk-synchronous phases over NVLink peer stores,
+        xchg_kernel.cu; default), 'fused' (per-CTA round trips,
+        shard_kernel.cu) or 'nccl' (the bulk protocol with host-driven
+        ncclSend/ncclRecv -- the measured baseline); all exact."""
+        check(lib.dvsg_set_shard_exchange(self._h, {"bulk": 0, "fused": 1, "nccl": 2}[mode]))
+
+    def nccl_unique_id(self) -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib.dvsg_nccl_unique_id(self._h, buf))
+        return buf.raw
+
+    def nccl_connect(self, uid: bytes) -> None:
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        check(lib.dvsg_nccl_connect(self._h, buf))
 
     def shard_prepare(self) -> None:
         check(lib.dvsg_shard_prepare(self._h))

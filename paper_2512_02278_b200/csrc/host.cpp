@@ -28,6 +28,8 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "../../include/dvsg.h"
 #include "dvsg_internal.h"
@@ -177,11 +179,15 @@ struct dvsg_ctx {
     DevBuf<dvsg::XgView> d_views;
     DevBuf<unsigned long long> counters;
     DevBuf<int> err;
+    std::vector<size_t> nccl_send, nccl_recv;  // this phase's request counts per peer
     unsigned epoch[4] = {0, 0, 0, 0};
     bool issued = false;
   } xg;
 
-  int shard_exchange = -1;                     // 0 bulk (default), 1 fused; -1: env DVSG_SHARD_EXCHANGE
+  int shard_exchange = -1;                     // 0 bulk (default), 1 fused, 2 nccl; -1: env DVSG_SHARD_EXCHANGE
+  // NCCL baseline of the bulk exchange (host-driven send/recv per phase)
+  ncclComm_t nccl = nullptr;
+  DevBuf<unsigned char> nccl_buf;
   DevBuf<unsigned char> emu_arena;             // emulation: all virtual ranks' arenas
   DevBuf<dvsg::ShardView> d_views;
   DevBuf<uint32_t> iota_q, zero_p;
@@ -548,6 +554,44 @@ void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uin
   c->launches += 1;
 }
 
+// ---- NCCL, loaded at run time (the process's libnccl.so.2, e.g. torch's) ---
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+    a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    return a;
+  }();
+  if (!api.send || !api.comm_init_rank) fail(DVSG_EINTERNAL, "NCCL exchange: libnccl.so.2 not loadable");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    fail(DVSG_EINTERNAL, "%s: NCCL error %d (%s)", what, (int)r,
+         nccl_api().error_string ? nccl_api().error_string(r) : "?");
+}
+
 // ---- node-sharded search, bulk-synchronous exchange (xchg_kernel.cu) -------
 constexpr size_t kXgHeader = 256;  // cursor [2][8] u32 @0, flags [8] u32 @64
 constexpr int kXgLanes = 4;
@@ -621,14 +665,21 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
     if (!c->sh.connected) fail(DVSG_EINVAL, "sharded search: call dvsg_shard_init and dvsg_shard_connect first");
     if (nranks != c->sh.nranks) fail(DVSG_EINVAL, "sharded search: nranks %d != %d", nranks, c->sh.nranks);
   }
+  // NCCL baseline: same kernels over local send/receive slabs, exchanged by
+  // host-driven ncclSend/ncclRecv after each half-phase (counts via the host)
+  const bool use_nccl = !emulate && c->shard_exchange == 2;
+  if (use_nccl && !c->nccl) fail(DVSG_EINVAL, "NCCL exchange: call dvsg_nccl_connect first");
   // lanes and wave size (comm region + origin state budgets, split per lane)
-  const int L = (int)std::max<uint64_t>(1, std::min<uint64_t>(kXgLanes, env_u64("DVSG_XG_LANES", 2)));
+  const int L = use_nccl ? 1 : (int)std::max<uint64_t>(1, std::min<uint64_t>(kXgLanes, env_u64("DVSG_XG_LANES", 2)));
   const uint64_t comm_q = (uint64_t)R * ((uint64_t)c->dpad * 4 + 16 * maxraw);
   const uint64_t state_q = k.cap * 8 + k.hsize * 4 + 16 + 8 * (uint64_t)R;
   const size_t lane_bytes = emulate ? 0 : ((c->sh.xg_bytes / (size_t)L) & ~(size_t)4095);
   uint64_t wmax = upr;
   if (emulate) {
     wmax = std::min<uint64_t>(wmax, std::max<uint64_t>(1, (env_u64("DVSG_XG_EMU_MB", 2048) << 20) / ((uint64_t)L * R * comm_q)));
+  } else if (use_nccl) {
+    const uint64_t per_q = (uint64_t)R * R * maxraw * 16 + (uint64_t)R * c->dpad * 4;
+    wmax = std::min<uint64_t>(wmax, std::max<uint64_t>(1, (env_u64("DVSG_XG_NCCL_MB", 16384) << 20) / per_q));
   } else {
     const uint64_t room = lane_bytes > kXgHeader + 512 ? (lane_bytes - kXgHeader - 512) / comm_q : 0;
     if (room < 1) fail(DVSG_EINVAL, "sharded search: comm arena too small for one query");
@@ -670,10 +721,41 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
         v.qall = x.emu_q.p + (size_t)l * R * wcap * (uint64_t)c->dpad;  // one copy stands in for every owner's
       }
   } else {
-    for (int l = 0; l < L; ++l)
+    for (int l = 0; l < L && !use_nccl; ++l)
       for (int r = 0; r < R; ++r)
         views[(size_t)l * R + r] = xg_view(c->sh.peers[(size_t)r] + c->sh.xg_off + (size_t)l * lane_bytes,
                                            r == me ? c->vec.p : nullptr, (uint64_t)r * S, R, wcap, maxraw, c->dpad);
+  }
+  // NCCL layout (all local): slab (o*R + s) of the request / reply arrays is
+  // "from origin s to owner o" / "from owner s to origin o"; with
+  // views[o].inbox = req + o*R*rstride the kernels' indexing (origin writes
+  // views[o].inbox + me*rstride, owner reads views[me].inbox + o*rstride)
+  // lands in send slab (o*R+me) and receive slab (me*R+o).  Cursors:
+  // views[o].cursor = cur + o*2R, so origin counters and received counts
+  // (written by ncclRecv) never collide.
+  uint64_t* n_req = nullptr;
+  uint64_t* n_rep = nullptr;
+  unsigned* n_cur = nullptr;
+  float* n_q = nullptr;
+  if (use_nccl) {
+    const size_t slabs = (size_t)R * R * rstride * 8;
+    const size_t qb = (size_t)R * wcap * (uint64_t)c->dpad * 4;
+    const size_t cb = (size_t)R * 2 * R * 4;
+    c->nccl_buf.reserve(2 * slabs + qb + cb + 1024, c->stream);
+    n_req = reinterpret_cast<uint64_t*>(c->nccl_buf.p);
+    n_rep = reinterpret_cast<uint64_t*>(c->nccl_buf.p + slabs);
+    n_q = reinterpret_cast<float*>(c->nccl_buf.p + 2 * slabs);
+    n_cur = reinterpret_cast<unsigned*>(c->nccl_buf.p + 2 * slabs + qb);
+    for (int o = 0; o < R; ++o) {
+      auto& v = views[(size_t)o];
+      v.vec = o == me ? c->vec.p : nullptr;
+      v.lo = (uint64_t)o * S;
+      v.cursor = n_cur + (size_t)o * 2 * R;
+      v.flags = nullptr;
+      v.qall = n_q;
+      v.inbox = n_req + (size_t)o * R * rstride;
+      v.reply = n_rep + (size_t)o * R * rstride;
+    }
   }
   x.d_views.reserve(views.size(), c->stream);
   cuda_check(cudaMemcpyAsync(x.d_views.p, views.data(), views.size() * sizeof(dvsg::XgView), cudaMemcpyHostToDevice, c->stream), "views");
@@ -717,7 +799,7 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
     la[l].meta = x.meta.p + so * (uint64_t)R;
   }
   auto barrier = [&](int l) {
-    if (emulate) return;  // stream order is the barrier
+    if (emulate || use_nccl) return;  // stream order (+ NCCL) is the barrier
     x.epoch[l] += 1;
     cuda_check(dvsg::launch_xg_barrier(la[l].views, R, me, x.epoch[l], x.err.p, c->stream), "xg barrier");
     c->launches += 1;
@@ -742,7 +824,7 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
         if (!a.wave_n[rr]) continue;
         const int o = me + rr;
         const float* src = d_q + ((emulate ? (uint64_t)o * upr : 0) + off) * (uint64_t)dim;
-        for (int r = 0; r < (emulate ? 1 : R); ++r) {
+        for (int r = 0; r < (emulate || use_nccl ? 1 : R); ++r) {
           float* dst = views[(size_t)l * R + r].qall + (uint64_t)o * wcap * (uint64_t)c->dpad;
           cuda_check(cudaMemcpy2DAsync(dst, (size_t)c->dpad * 4, src, (size_t)dim * 4, (size_t)dim * 4,
                                        a.wave_n[rr], cudaMemcpyDefault, c->stream), "push queries");
@@ -752,6 +834,17 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
       a.out_dists = d_dists + off * (uint64_t)p->k;
       a.out_count = d_count + off;
       a.out_visited = d_visited + off;
+      if (use_nccl) {  // all-gather of the wave's queries (every rank has the same wave size)
+        const NcclApi& nc = nccl_api();
+        const size_t qn = (size_t)a.wave_n[0] * (uint64_t)c->dpad;
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        for (int o = 0; o < R; ++o) {
+          if (o == me) continue;
+          nccl_check(nc.send(n_q + (size_t)me * wcap * c->dpad, qn, ncclFloat32, o, c->nccl, c->stream), "ncclSend");
+          nccl_check(nc.recv(n_q + (size_t)o * wcap * c->dpad, qn, ncclFloat32, o, c->nccl, c->stream), "ncclRecv");
+        }
+        nccl_check(nc.group_end(), "ncclGroupEnd");
+      }
       barrier(l);  // every owner holds this wave's queries
     }
     cuda_check(cudaMemsetAsync(x.counters.p, 0, 2 * (size_t)nlaunch * sizeof(unsigned long long), c->stream), "counters");
@@ -768,18 +861,64 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
           la[l].phase = op >> 1;
         }
       }
-      const dvsg::XgArgs& ea = la[le >= 0 ? le : ls];
-      const dvsg::XgArgs& sa = la[ls >= 0 ? ls : le];
+      const dvsg::XgArgs& ea = la[std::max(0, le >= 0 ? le : ls)];
+      const dvsg::XgArgs& sa = la[std::max(0, ls >= 0 ? ls : le)];
+      if (use_nccl && le >= 0)
+        cuda_check(cudaMemsetAsync(n_cur, 0, (size_t)R * 2 * R * 4, c->stream), "cursor reset");
       cuda_check(dvsg::launch_xg_step(ea, sa, le >= 0, ls >= 0, x.counters.p + 2 * t, p->metric, p->accum,
                                       c->num_sms, c->stream), "xg step");
       c->launches += 1;
-      if (ls >= 0)  // that phase's inbox cursors are free again (next used two barriers later)
+      if (ls >= 0 && !use_nccl)  // that phase's inbox cursors are free again (next used two barriers later)
         for (int rr = 0; rr < rank_n; ++rr)
           cuda_check(cudaMemsetAsync(views[(size_t)ls * R + me + rr].cursor + (la[ls].phase & 1) * R, 0,
                                      (size_t)R * 4, c->stream), "cursor reset");
       // requests (after an expand) / replies (after a score) delivered
       if (le >= 0 && la[le].phase <= p->iterations) barrier(le);
       if (ls >= 0) barrier(ls);
+      if (use_nccl && le >= 0 && la[le].phase <= p->iterations) {
+        // requests: counts through the host (NCCL needs host-side sizes), then data
+        const NcclApi& nc = nccl_api();
+        const int slot = la[le].phase & 1;
+        std::vector<unsigned> cur((size_t)R * 2 * R);
+        cuda_check(cudaMemcpyAsync(cur.data(), n_cur, cur.size() * 4, cudaMemcpyDeviceToHost, c->stream), "counts");
+        cuda_check(cudaStreamSynchronize(c->stream), "counts");
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        for (int o = 0; o < R; ++o) {
+          if (o == me) continue;
+          nccl_check(nc.send(n_cur + (size_t)o * 2 * R + slot * R + me, 1, ncclUint32, o, c->nccl, c->stream), "ncclSend");
+          nccl_check(nc.recv(n_cur + (size_t)me * 2 * R + slot * R + o, 1, ncclUint32, o, c->nccl, c->stream), "ncclRecv");
+        }
+        nccl_check(nc.group_end(), "ncclGroupEnd");
+        cuda_check(cudaMemcpyAsync(cur.data(), n_cur, cur.size() * 4, cudaMemcpyDeviceToHost, c->stream), "counts");
+        cuda_check(cudaStreamSynchronize(c->stream), "counts");
+        x.nccl_send.assign((size_t)R, 0);
+        x.nccl_recv.assign((size_t)R, 0);
+        for (int o = 0; o < R; ++o) {
+          x.nccl_send[(size_t)o] = cur[(size_t)o * 2 * R + slot * R + me];
+          x.nccl_recv[(size_t)o] = cur[(size_t)me * 2 * R + slot * R + o];
+        }
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        for (int o = 0; o < R; ++o) {
+          if (o == me) continue;
+          if (x.nccl_send[(size_t)o])
+            nccl_check(nc.send(n_req + ((size_t)o * R + me) * rstride, x.nccl_send[(size_t)o], ncclUint64, o, c->nccl, c->stream), "ncclSend");
+          if (x.nccl_recv[(size_t)o])
+            nccl_check(nc.recv(n_req + ((size_t)me * R + o) * rstride, x.nccl_recv[(size_t)o], ncclUint64, o, c->nccl, c->stream), "ncclRecv");
+        }
+        nccl_check(nc.group_end(), "ncclGroupEnd");
+      }
+      if (use_nccl && ls >= 0) {  // replies: the same counts, reversed
+        const NcclApi& nc = nccl_api();
+        nccl_check(nc.group_start(), "ncclGroupStart");
+        for (int o = 0; o < R; ++o) {
+          if (o == me) continue;
+          if (x.nccl_recv[(size_t)o])
+            nccl_check(nc.send(n_rep + ((size_t)o * R + me) * rstride, x.nccl_recv[(size_t)o], ncclUint64, o, c->nccl, c->stream), "ncclSend");
+          if (x.nccl_send[(size_t)o])
+            nccl_check(nc.recv(n_rep + ((size_t)me * R + o) * rstride, x.nccl_send[(size_t)o], ncclUint64, o, c->nccl, c->stream), "ncclRecv");
+        }
+        nccl_check(nc.group_end(), "ncclGroupEnd");
+      }
     }
   }
   if (c->timing) {
@@ -792,9 +931,9 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
 bool use_bulk_exchange(dvsg_ctx* c) {
   if (c->shard_exchange < 0) {
     const char* e = std::getenv("DVSG_SHARD_EXCHANGE");
-    c->shard_exchange = (e && std::strcmp(e, "fused") == 0) ? 1 : 0;
+    c->shard_exchange = (e && std::strcmp(e, "fused") == 0) ? 1 : (e && std::strcmp(e, "nccl") == 0) ? 2 : 0;
   }
-  return c->shard_exchange == 0;
+  return c->shard_exchange != 1;
 }
 
 template <class T>
@@ -992,6 +1131,7 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     for (size_t r = 0; r < c->sh.peers.size(); ++r)
       if ((int)r != c->sh.rank && c->sh.peers[r]) cudaIpcCloseMemHandle(c->sh.peers[r]);
     if (c->sh.arena) cudaFree(c->sh.arena);
+    if (c->nccl) nccl_api().comm_destroy(c->nccl);
     for (auto& e : c->ev) cudaEventDestroy(e);
     for (auto& e : c->mb_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
@@ -1552,8 +1692,31 @@ dvsg_status dvsg_brute_force_topk(dvsg_ctx* c, const float* db, uint64_t n, int 
 
 dvsg_status dvsg_set_shard_exchange(dvsg_ctx* c, int mode) {
   return guarded([&] {
-    if (mode != 0 && mode != 1) fail(DVSG_EINVAL, "set_shard_exchange: mode %d (0 bulk, 1 fused)", mode);
+    if (mode < 0 || mode > 2) fail(DVSG_EINVAL, "set_shard_exchange: mode %d (0 bulk, 1 fused, 2 nccl)", mode);
     c->shard_exchange = mode;
+  });
+}
+
+dvsg_status dvsg_nccl_unique_id(dvsg_ctx* c, void* out128) {
+  return guarded([&] {
+    (void)c;
+    ncclUniqueId id;
+    nccl_check(nccl_api().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+dvsg_status dvsg_nccl_connect(dvsg_ctx* c, const void* id128) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->sh.active) fail(DVSG_EINVAL, "nccl_connect: call dvsg_shard_init first");
+    if (c->nccl) {
+      nccl_api().comm_destroy(c->nccl);
+      c->nccl = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    nccl_check(nccl_api().comm_init_rank(&c->nccl, c->sh.nranks, id, c->sh.rank), "ncclCommInitRank");
   });
 }
 

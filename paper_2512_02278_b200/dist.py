@@ -49,6 +49,15 @@ def setup_sharded(ctx, rank: int, nranks: int, data, adjacency, entry_order,
     return lo, hi
 
 
+def connect_nccl(ctx, rank: int, group=None) -> None:
+    """NCCL communicator for the 'nccl' exchange: rank 0's unique id is
+    broadcast over torch.distributed (control plane only)."""
+    import torch.distributed as dist
+    box = [ctx.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    ctx.nccl_connect(box[0])
+
+
 def prepare_step(ctx, barrier) -> None:
     """Reset this rank's arena; no rank may launch before every reset is done."""
     ctx.shard_prepare()
