@@ -197,6 +197,20 @@ dvsg_status dvsg_combine_results(dvsg_ctx *ctx, uint64_t nq, int nparts, const u
                                  const float *dists, const uint32_t *counts, int stride, int k,
                                  uint32_t *out_ids, float *out_dists, uint32_t *out_count);
 
+/* Device-pointer variants (asynchronous on the compute stream; combine
+ * synchronizes to report an unsorted partial), used by the multi-GPU
+ * cluster-sharded pipeline (paper_2512_02278_b200/dist.py,
+ * run_pipeline_distributed).  gather_vectors: hit vectors of n result lists
+ * (k ids each, counts[i] valid) from the resident partitions, n x k x dim. */
+dvsg_status dvsg_assign_top_c_device(dvsg_ctx *ctx, const float *d_queries, uint64_t nq, int dim,
+                                     int c, uint32_t *d_out);
+dvsg_status dvsg_combine_results_device(dvsg_ctx *ctx, uint64_t nq, int nparts, const uint32_t *d_ids,
+                                        const float *d_dists, const uint32_t *d_counts, int stride,
+                                        int k, uint32_t *d_out_ids, float *d_out_dists,
+                                        uint32_t *d_out_count);
+dvsg_status dvsg_gather_vectors_device(dvsg_ctx *ctx, const uint32_t *d_ids, const uint32_t *d_counts,
+                                       uint64_t n, int k, float *d_out);
+
 /* ---- run_pipeline functional part (simulator.cpp:245-337), one GPU ------
  * assign (K5) -> route -> search (K1) -> combine (K4) -> attach hit vectors.
  * All clusters must be resident on this context.  Host buffers;

@@ -77,6 +77,10 @@ _SIGS = {
     "dvsg_build_graph": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
     "dvsg_brute_force_topk": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_uint64, c_int,
                                       c_void_p, c_void_p]),
+    "dvsg_assign_top_c_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
+    "dvsg_combine_results_device": (c_int, [c_void_p, c_uint64, c_int, c_void_p, c_void_p, c_void_p,
+                                            c_int, c_int, c_void_p, c_void_p, c_void_p]),
+    "dvsg_gather_vectors_device": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64, c_int, c_void_p]),
     "dvsg_set_shard_exchange": (c_int, [c_void_p, c_int]),
     "dvsg_nccl_unique_id": (c_int, [c_void_p, c_void_p]),
     "dvsg_nccl_connect": (c_int, [c_void_p, c_void_p]),

@@ -383,6 +383,30 @@ class Context:
                                            ctypes.c_void_p(d_vectors or None),
                                            ctypes.c_void_p(d_visited or None)))
 
+    # ---- device-pointer building blocks (asynchronous on self.stream) ------------
+    def search_units_device(self, d_queries: int, nq: int, dim: int, d_unit_query: int,
+                            d_unit_cluster: int, nunits: int, p: SearchParams, d_ids: int,
+                            d_dists: int, d_counts: int, d_visited: int) -> None:
+        cp = p.to_c()
+        v = ctypes.c_void_p
+        check(lib.dvsg_search_units_device(self._h, v(d_queries), int(nq), int(dim), v(d_unit_query),
+                                           v(d_unit_cluster), int(nunits), ctypes.byref(cp), v(d_ids),
+                                           v(d_dists), v(d_counts), v(d_visited)))
+
+    def assign_top_c_device(self, d_queries: int, nq: int, dim: int, c: int, d_out: int) -> None:
+        check(lib.dvsg_assign_top_c_device(self._h, ctypes.c_void_p(d_queries), int(nq), int(dim), int(c),
+                                           ctypes.c_void_p(d_out)))
+
+    def combine_results_device(self, nq: int, nparts: int, d_ids: int, d_dists: int, d_counts: int,
+                               stride: int, k: int, d_out_ids: int, d_out_dists: int, d_out_count: int) -> None:
+        v = ctypes.c_void_p
+        check(lib.dvsg_combine_results_device(self._h, int(nq), int(nparts), v(d_ids), v(d_dists), v(d_counts),
+                                              int(stride), int(k), v(d_out_ids), v(d_out_dists), v(d_out_count)))
+
+    def gather_vectors_device(self, d_ids: int, d_counts: int, n: int, k: int, d_out: int) -> None:
+        v = ctypes.c_void_p
+        check(lib.dvsg_gather_vectors_device(self._h, v(d_ids), v(d_counts), int(n), int(k), v(d_out)))
+
     def brute_force_topk(self, db, queries, k: int):
         """topk.cpp:12-30 on the GPU -> (ids nq x k, dists nq x k)."""
         d = _f32(db, 2)

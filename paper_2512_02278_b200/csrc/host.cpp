@@ -1496,6 +1496,49 @@ dvsg_status dvsg_assign_top_c(dvsg_ctx* c, const float* queries, uint64_t nq, in
   });
 }
 
+dvsg_status dvsg_assign_top_c_device(dvsg_ctx* c, const float* d_queries, uint64_t nq, int dim, int cc,
+                                     uint32_t* d_out) {
+  return guarded([&] {
+    set_device(c);
+    if (c->clusters < 1) fail(DVSG_EINVAL, "assign_top_c: empty centroids");
+    if (cc < 1 || cc > c->clusters) fail(DVSG_EINVAL, "assign_top_c: c=%d out of range for %d clusters", cc, c->clusters);
+    if (dim != c->dim) fail(DVSG_EINVAL, "assign_top_c: query dim %d != centroid dim %d", dim, c->dim);
+    if (nq == 0) return;
+    c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
+    cuda_check(dvsg::launch_assign(d_queries, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, d_out, c->assign_scratch.p, c->stream), "assign");
+    c->launches += 1;
+  });
+}
+
+dvsg_status dvsg_combine_results_device(dvsg_ctx* c, uint64_t nq, int nparts, const uint32_t* d_ids,
+                                        const float* d_dists, const uint32_t* d_counts, int stride, int k,
+                                        uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_count) {
+  return guarded([&] {
+    set_device(c);
+    if (k < 1) fail(DVSG_EINVAL, "combine_results: k must be >= 1");
+    if (nparts < 1 || nparts > 32) fail(DVSG_EINVAL, "combine_results: %d partials outside the device merge width 1..32", nparts);
+    if (stride < k) fail(DVSG_EINVAL, "combine_results: stride %d below k %d", stride, k);
+    if (nq == 0) return;
+    c->err_flag.reserve(1, c->stream);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+    cuda_check(dvsg::launch_combine(nq, nparts, d_ids, d_dists, d_counts, stride, k, d_out_ids, d_out_dists, d_out_count, c->err_flag.p, c->stream), "combine");
+    c->launches += 1;
+    check_err_flag(c, "combine_results: partial list not sorted by (dist, id)");
+  });
+}
+
+dvsg_status dvsg_gather_vectors_device(dvsg_ctx* c, const uint32_t* d_ids, const uint32_t* d_counts,
+                                       uint64_t n, int k, float* d_out) {
+  return guarded([&] {
+    set_device(c);
+    if (c->parts.empty()) fail(DVSG_EINVAL, "gather_vectors: no resident partition");
+    if (n == 0) return;
+    build_locator(c);
+    cuda_check(dvsg::launch_gather_vectors(d_ids, d_counts, n, k, c->d_locator.p, c->vec.p, c->dim, c->dpad, d_out, c->stream), "gather vectors");
+    c->launches += 1;
+  });
+}
+
 dvsg_status dvsg_combine_results(dvsg_ctx* c, uint64_t nq, int nparts, const uint32_t* ids,
                                  const float* dists, const uint32_t* counts, int stride, int k,
                                  uint32_t* out_ids, float* out_dists, uint32_t* out_count) {

@@ -1,12 +1,19 @@
-"""Multi-GPU plumbing for the node-sharded search (one process per GPU).
+"""Multi-GPU plumbing (one process per GPU).
 
-torch.distributed carries only control-plane data here: the 64-byte CUDA IPC
-handles of each rank's comm arena (all_gather_object) and barriers.  The data
-path -- candidate ids out, scored keys back -- is the fused kernel's own
-NVLink peer stores (shard_kernel.cu), not a collective.
-
+Node-sharded search (SURVEY 8e design B): torch.distributed carries only
+control-plane data -- the 64-byte CUDA IPC handles of each rank's comm arena
+(all_gather_object), the NCCL unique id of the baseline exchange, barriers.
+The data path -- candidate ids out, scored keys back -- is the kernels' own
+NVLink peer stores (xchg_kernel.cu / shard_kernel.cu), not a collective.
 The shard rule is the C-ABI's (dvsg_shard_init): S = ceil(n / R), rank r owns
 node ids [r*S, min(n, (r+1)*S)).
+
+Cluster-sharded pipeline (SURVEY 8e design A, the reference's own
+run_pipeline semantics across ranks): run_pipeline_distributed below --
+cluster i lives on rank placement[i] (router.cpp:38-41), one all-to-all
+dispatches the routed (query, cluster) units to their owners and one sends
+the results back (NCCL through torch.distributed), the library kernels do
+the assignment, the per-partition searches and the combine.
 """
 from __future__ import annotations
 
@@ -66,3 +73,92 @@ def prepare_step(ctx, barrier) -> None:
 
 def split_even(n: int, parts: int) -> Sequence[Tuple[int, int]]:
     return [(n * i // parts, n * (i + 1) // parts) for i in range(parts)]
+
+
+def route_to_owners(assign, placement, world: int):
+    """router.cpp:52-79 over device tensors: unit u = q * fanout + j is routed
+    to rank placement[assign[q, j]] (self-traffic kept).  Returns (order,
+    send_counts): units grouped by owner rank (stable), and units per rank."""
+    import torch
+    owner = placement.index_select(0, assign.reshape(-1).long())
+    order = torch.argsort(owner, stable=True)
+    return order, torch.bincount(owner, minlength=world)
+
+
+def run_pipeline_distributed(ctx, d_q, p, fanout: int, placement, world: int, with_vectors: bool = True,
+                             group=None):
+    """run_pipeline (simulator.cpp:250-337), cluster-sharded across ranks.
+
+    ctx holds the centroids (set_centroids) and the partitions of the clusters
+    placed on this rank; d_q is this rank's query batch (torch, nq x dim, on
+    ctx's device); placement a device tensor cluster -> rank.  Returns torch
+    tensors (ids nq x k, dists, counts, vectors nq x k x dim or None) and the
+    batch's visited_total -- identical to a one-GPU run_pipeline over the same
+    queries with every cluster resident (tests, bench --mode cluster)."""
+    import torch
+    import torch.distributed as dist
+    dev = d_q.device
+    nq, dim = int(d_q.shape[0]), int(d_q.shape[1])
+    k, c = int(p.k), int(fanout)
+    cs = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    with torch.cuda.stream(cs):  # torch ops and library calls share one stream
+        assign = torch.empty((nq, c), dtype=torch.int32, device=dev)
+        ctx.assign_top_c_device(d_q.data_ptr(), nq, dim, c, assign.data_ptr())
+        order, send_counts = route_to_owners(assign, placement, world)
+        recv_counts = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        nrecv = int(sum(rc))
+        # dispatch: each routed unit carries its query vector and cluster id
+        q_send = d_q.index_select(0, torch.div(order, c, rounding_mode="floor"))
+        cl_send = assign.reshape(-1).index_select(0, order)
+        q_recv = torch.empty((nrecv, dim), dtype=d_q.dtype, device=dev)
+        cl_recv = torch.empty((nrecv,), dtype=torch.int32, device=dev)
+        dist.all_to_all_single(q_recv, q_send, rc, sc, group=group)
+        dist.all_to_all_single(cl_recv, cl_send, rc, sc, group=group)
+        # owner: search every received unit in its resident partition
+        r_ids = torch.empty((nrecv, k), dtype=torch.int32, device=dev)
+        r_d = torch.empty((nrecv, k), dtype=torch.float32, device=dev)
+        r_cnt = torch.empty((nrecv,), dtype=torch.int32, device=dev)
+        r_vis = torch.empty((nrecv,), dtype=torch.int64, device=dev)
+        if nrecv:
+            uq = torch.arange(nrecv, dtype=torch.int32, device=dev)
+            ctx.search_units_device(q_recv.data_ptr(), nrecv, dim, uq.data_ptr(), cl_recv.data_ptr(), nrecv, p,
+                                    r_ids.data_ptr(), r_d.data_ptr(), r_cnt.data_ptr(), r_vis.data_ptr())
+        r_vec = None
+        if with_vectors:
+            r_vec = torch.zeros((nrecv, k, dim), dtype=torch.float32, device=dev)
+            if nrecv:
+                ctx.gather_vectors_device(r_ids.data_ptr(), r_cnt.data_ptr(), nrecv, k, r_vec.data_ptr())
+        # combine all-to-all: results back to the origin, then un-permute
+        nu = nq * c
+
+        def back(t, shape):
+            out = torch.empty(shape, dtype=t.dtype, device=dev)
+            dist.all_to_all_single(out, t, sc, rc, group=group)
+            u = torch.empty_like(out)
+            u[order] = out
+            return u
+
+        u_ids = back(r_ids, (nu, k))
+        u_d = back(r_d, (nu, k))
+        u_cnt = back(r_cnt, (nu,))
+        u_vis = back(r_vis, (nu,))
+        ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        counts = torch.empty((nq,), dtype=torch.int32, device=dev)
+        ctx.combine_results_device(nq, c, u_ids.data_ptr(), u_d.data_ptr(), u_cnt.data_ptr(), k, k,
+                                   ids.data_ptr(), dists.data_ptr(), counts.data_ptr())
+        vectors = None
+        if with_vectors:
+            u_vec = back(r_vec, (nu, k, dim)).view(nq, c * k, dim)
+            # each final hit comes from exactly one partial slot (clusters are disjoint)
+            part_ids = u_ids.view(nq, c * k)
+            slot_ok = (torch.arange(k, device=dev)[None, None, :] < u_cnt.view(nq, c, 1)).view(nq, c * k)
+            hit_ok = torch.arange(k, device=dev)[None, :] < counts[:, None]
+            match = (part_ids[:, None, :] == ids[:, :, None]) & slot_ok[:, None, :]
+            src = match.int().argmax(dim=2)
+            vectors = torch.gather(u_vec, 1, src[:, :, None].expand(nq, k, dim))
+            vectors = torch.where(hit_ok[:, :, None], vectors, torch.zeros_like(vectors))
+        visited_total = int(u_vis.sum().item())
+    return ids, dists, counts, vectors, visited_total

@@ -1,0 +1,110 @@
+"""Cluster-sharded run_pipeline across GPUs (SURVEY 8e design A): parity with
+the one-GPU pipeline over the same queries, then timing.
+
+    torchrun --nproc-per-node N scripts/cluster_pipeline_mgpu.py [--rows 1000000]
+        [--clusters-per-gpu 2] [--fanout 2] [--nq 100000] [--steps 3]
+
+Every rank builds the same k-means index (synth.build_index, C = N x
+clusters-per-gpu, cluster i on rank i mod N), keeps only its own clusters'
+partitions for the distributed run, and checks ids / dists / counts / hit
+vectors / visited_total against ctx.run_pipeline on a context holding every
+cluster.  Rank 0 prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", type=int, default=1_000_000)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--clusters-per-gpu", type=int, default=2)
+    ap.add_argument("--fanout", type=int, default=2)
+    ap.add_argument("--nq", type=int, default=100_000)
+    ap.add_argument("--check", type=int, default=20_000)
+    ap.add_argument("--beam", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    import paper_2512_02278_b200 as dvs
+    from paper_2512_02278_b200 import synth
+    from paper_2512_02278_b200.dist import run_pipeline_distributed
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    data = synth.sift_like(a.rows, a.dim, 16, seed=1)
+    clusters = world * a.clusters_per_gpu
+    full = dvs.Context(local)
+    index = synth.build_index(full, data, clusters, out_degree=32, ranks=world)
+    full.load_index(index)
+    ctx = dvs.Context(local)
+    ctx.load_index(index, rank=rank)
+    placement = torch.from_numpy(index.cluster_to_rank.astype(np.int64)).to(dev)
+    queries = synth.sift_like_queries(a.nq, a.dim, 16, data_seed=1, seed=2 + rank)
+    p = dvs.SearchParams(6, a.beam, 10, a.beam, accum="f32")
+    setup_s = time.time() - t0
+
+    # parity on the first `check` queries
+    qc = queries[:a.check]
+    want = full.run_pipeline(qc, p, a.fanout, world)
+    ids, dists, counts, vecs, vt = run_pipeline_distributed(ctx, torch.from_numpy(qc).to(dev), p, a.fanout,
+                                                            placement, world)
+    ctx.synchronize()
+    cnt = counts.cpu().numpy().view(np.uint32)
+    ok = bool(np.array_equal(cnt, want.counts) and vt == want.visited_total)
+    gi, gd, gv = ids.cpu().numpy().view(np.uint32), dists.cpu().numpy(), vecs.cpu().numpy()
+    for q in range(qc.shape[0]):
+        n = int(want.counts[q])
+        if not (np.array_equal(gi[q, :n], want.ids[q, :n]) and np.array_equal(gd[q, :n], want.dists[q, :n])
+                and np.array_equal(gv[q, :n], want.hit_vectors[q, :n])):
+            ok = False
+            break
+    same = torch.tensor([int(ok)], device=dev)
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+
+    # timing: the whole distributed pipeline on device-resident queries
+    d_q = torch.from_numpy(queries).to(dev)
+    for _ in range(2):
+        run_pipeline_distributed(ctx, d_q, p, a.fanout, placement, world)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    e0.record(stream)
+    vis = 0
+    for _ in range(a.steps):
+        vis += run_pipeline_distributed(ctx, d_q, p, a.fanout, placement, world)[4]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # recall on this rank's first 1000 queries
+    truth = synth.brute_force_gt(data, queries[:1000], 10, ctx=full)
+    rec = synth.recall_at_k(ids.cpu().numpy().view(np.uint32)[:1000], cnt[:1000], truth, 10)
+    if rank == 0:
+        ms = float(t[0]) / a.steps
+        print(json.dumps({
+            "mode": "cluster-sharded run_pipeline (design A)", "n_gpus": world, "n": a.rows, "dim": a.dim,
+            "clusters": clusters, "fanout": a.fanout, "beam": a.beam, "queries_per_gpu": a.nq,
+            "qps": a.nq * world / (ms / 1e3), "ms_per_step": ms, "visited_per_query": vis / a.steps / a.nq,
+            "recall_at_10_rank0": round(rec, 4), "identical_to_one_gpu_pipeline_all_ranks": bool(same[0]),
+            "checked_queries_per_rank": a.check, "setup_s": round(setup_s, 1),
+            "exchange": "NCCL all_to_all_single (torch.distributed): dispatch of (query, cluster) units, "
+                        "results + hit vectors back"}), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -87,3 +87,19 @@ def test_setup_sharded_two_ranks_gloo():
         calls = out[r][2]
         assert calls[0] == ("init", 2, r, 501 if r == 0 else 500, 1001)
         assert calls[1] == ("connect", [0, 1])  # every rank's handle, in rank order
+
+
+def test_route_to_owners_matches_router_semantics():
+    """router.cpp:52-79 (design A dispatch): every (query, slot) unit goes to
+    placement[cluster]; units grouped by owner rank, stable within a rank."""
+    import torch
+    from paper_2512_02278_b200.dist import route_to_owners
+    rng = np.random.default_rng(3)
+    nq, fanout, clusters, world = 257, 3, 12, 4
+    assign = torch.from_numpy(rng.integers(0, clusters, size=(nq, fanout)).astype(np.int32))
+    placement = torch.from_numpy((np.arange(clusters) % world).astype(np.int64))  # place_clusters, router.cpp:38-41
+    order, counts = route_to_owners(assign, placement, world)
+    owner = (assign.numpy().reshape(-1) % world)
+    want = [u for r in range(world) for u in range(nq * fanout) if owner[u] == r]
+    assert order.tolist() == want
+    assert counts.tolist() == [int((owner == r).sum()) for r in range(world)]
