@@ -282,6 +282,46 @@ def test_pipeline_matches_reference_golden(ctx, golden):
         ctx.run_pipeline(q, dvs.SearchParams(6, 16, 10, 16), 2, 8)
 
 
+def test_device_entry_points_and_distributed_pipeline_single_rank(ctx, golden):
+    """assign/combine/gather device entry points and the cluster-sharded
+    pipeline's route -> search -> return -> combine path (one NCCL rank)
+    reproduce the reference's run_pipeline golden."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from fnsy import G3_FNSY
+    from paper_2512_02278_b200.dist import run_pipeline_distributed
+    res = golden("g3_mixture.npz")
+    dvs.load_index(G3_FNSY, ctx=ctx)
+    q = res["queries"]
+    dev = torch.device("cuda", 0)
+    d_q = torch.from_numpy(q).to(dev)
+    out = torch.empty((len(q), 3), dtype=torch.int32, device=dev)
+    ctx.assign_top_c_device(d_q.data_ptr(), len(q), q.shape[1], 3, out.data_ptr())
+    ctx.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ctx.assign_top_c(q, 3))
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=dev)
+    placement = torch.zeros(8, dtype=torch.int64, device=dev)
+    for fo in (1, 2, 3):
+        ids, dists, counts, vecs, vt = run_pipeline_distributed(ctx, d_q, dvs.SearchParams(6, 16, 10, 16), fo,
+                                                                placement, 1)
+        ctx.synchronize()
+        cnt = counts.cpu().numpy().view(np.uint32)
+        assert np.array_equal(cnt, res[f"counts_f{fo}"])
+        gi, gd, gv = ids.cpu().numpy().view(np.uint32), dists.cpu().numpy(), vecs.cpu().numpy()
+        for i in range(len(q)):
+            n = int(cnt[i])
+            assert np.array_equal(gi[i, :n], res[f"ids_f{fo}"][i, :n])
+            assert np.array_equal(gd[i, :n], res[f"dists_f{fo}"][i, :n])
+            assert np.array_equal(gv[i, :n], res[f"vectors_f{fo}"][i, :n])
+        assert vt == int(res[f"visited_f{fo}"])
+
+
 def test_load_index_rank_filter(ctx):
     from fnsy import G3_FNSY, read_fnsy
     idx = read_fnsy(G3_FNSY)
