@@ -36,6 +36,9 @@ struct SearchArgs {
   int iters, beam, k, entry_count, cap;
   int chp;      // survivor buffer entries (pow2 >= max(chunk, cap))
   int hsize;    // visited hash slots (pow2)
+  int hsmall;   // K1, global hash: > 0 -> start each unit in a hsmall-slot table and
+                // move to the full hsize one only when the load could pass 3/4
+                // (per-CTA region = hsmall + hsize slots); 0 -> full table
   uint32_t* hash_global;  // nullptr -> visited hash in shared memory
   uint32_t* out_ids;      // nunits x k
   float* out_dists;       // nunits x k

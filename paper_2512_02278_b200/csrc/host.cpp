@@ -421,7 +421,12 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
       return e ? std::strtoull(e, nullptr, 10) << 20 : 0ull;
     }();
     if (l2_budget) max_grid = (int)std::max<uint64_t>((uint64_t)c->num_sms, std::min<uint64_t>((uint64_t)max_grid, l2_budget / (4 * k.hsize)));
-    c->hash.reserve((uint64_t)max_grid * k.hsize, c->stream);
+    // large beams: the worst-case tables (256 KB/CTA at w=256) stop fitting
+    // in L2; start every unit in a half-size table and grow exactly on demand
+    // (DVSG_HASH_SMALL_MIN: smallest full table that gets a small one; tests lower it)
+    const uint64_t small_min = env_u64("DVSG_HASH_SMALL_MIN", 65536);
+    a.hsmall = small_min && k.hsize >= small_min && k.hsize >= 128 ? (int)(k.hsize / 2) : 0;
+    c->hash.reserve((uint64_t)max_grid * (k.hsize + (uint64_t)a.hsmall), c->stream);
     a.hash_global = c->hash.p;
   }
   if (c->timing) cudaEventRecord(c->ev[0], c->stream);

@@ -58,9 +58,8 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   uint64_t* surv = pool_alt + a.cap;
   uint32_t* cand = reinterpret_cast<uint32_t*>(surv + a.chp);
   uint32_t* frontier = cand + kChunk;
-  uint32_t* table = a.hash_global ? a.hash_global + (size_t)blockIdx.x * (size_t)a.hsize
-                                  : frontier + ((a.beam + 3) & ~3);
-  const uint32_t hmask = (uint32_t)a.hsize - 1u;
+  uint32_t* const region = a.hash_global ? a.hash_global + (size_t)blockIdx.x * (size_t)(a.hsize + a.hsmall)
+                                         : frontier + ((a.beam + 3) & ~3);
   const uint32_t dg_magic = (uint32_t)((0x100000000ull + (uint64_t)a.dg - 1) / (uint64_t)a.dg);
   const unsigned full = 0xFFFFFFFFu;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -97,7 +96,12 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
       }
     }
 
-    for (int i = tid; i < a.hsize; i += kThreads) table[i] = kEmpty;
+    // visited table: the small one first when enabled (its lines stay in L2
+    // at large beams), the full one only when it could pass 3/4 load
+    uint32_t* table = region;
+    uint32_t hmask = (uint32_t)(a.hsmall ? a.hsmall : a.hsize) - 1u;
+    bool small = a.hsmall > 0;
+    for (int i = tid; i <= (int)hmask; i += kThreads) table[i] = kEmpty;
     __syncthreads();
 
     int P = 0;
@@ -148,6 +152,20 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
 
       for (int cbase = 0; cbase < raw_total; cbase += kChunk) {
         const int rcount = raw_total - cbase < kChunk ? raw_total - cbase : kChunk;
+        if (small && visited + (uint64_t)rcount > (uint64_t)(a.hsmall / 4 * 3)) {  // block-uniform
+          // exact growth: rehash the small table's ids into the full one
+          uint32_t* big = region + a.hsmall;
+          for (int i = tid; i < a.hsize; i += kThreads) big[i] = kEmpty;
+          __syncthreads();
+          for (int i = tid; i < a.hsmall; i += kThreads) {
+            const uint32_t v = table[i];
+            if (v != kEmpty) visit_insert(big, (uint32_t)a.hsize - 1u, v);
+          }
+          __syncthreads();
+          table = big;
+          hmask = (uint32_t)a.hsize - 1u;
+          small = false;
+        }
         if (tid == 0) {
           st.ncand = 0;
           st.nsurv = 0;

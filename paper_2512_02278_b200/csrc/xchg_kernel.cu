@@ -530,7 +530,10 @@ xg_step(const XgArgs ea, const XgArgs sa, int do_e, int do_s, unsigned long long
   const uint64_t nwb = do_s ? tab.pref[tab.nseg] : 0;  // score warp blocks
   // CTAs alternate a preferred kind (so every SM runs both), then help with
   // the other kind; expand items are per CTA, score blocks per warp.
-  const bool prefer_s = do_s && (!do_e || (blockIdx.x & 1));
+#ifndef DVSG_XG_S_EIGHTHS
+#define DVSG_XG_S_EIGHTHS 4  // eighths of the CTAs that start on score blocks
+#endif
+  const bool prefer_s = do_s && (!do_e || (int)(blockIdx.x & 7) < DVSG_XG_S_EIGHTHS);
   for (int pass = 0; pass < 2; ++pass) {
     const bool s_mode = (pass == 0) == prefer_s;
     if (s_mode) {

@@ -110,6 +110,24 @@ def test_pool_truncation_exact_under_ties(ctx, oracle, gid_order, I, w, k, E):
     _assert_same(got, want, True, (gid_order, "bulk sharded"))
 
 
+@pytest.mark.parametrize("small_min", ["128", "0"])
+def test_small_visited_table_growth_exact(ctx, oracle, monkeypatch, small_min):
+    """Visited tables that start at half size and grow (exact rehash) when
+    the load could pass 3/4 -- forced on small partitions -- give the
+    reference's results and visited counters."""
+    monkeypatch.setenv("DVSG_HASH_SMALL_MIN", small_min)
+    n, dim = 6000, 16
+    v = sift_like(n, dim, 6, 71)
+    adj = oracle.build_graph(v, 24)
+    eo = oracle.compute_entry_order(v)
+    q = sift_like(48, dim, 6, 72)
+    gids = np.arange(n, dtype=np.uint32)
+    for (I, w, k, E) in [(6, 64, 10, 64), (3, 128, 20, 300), (2, 8, 5, 8)]:
+        want = oracle.beam_search(v, gids, adj, eo, q, I, w, k, E)
+        got = _search(ctx, v, adj, q, dvs.SearchParams(I, w, k, E, accum="f32"), gids)
+        _assert_same(got, want, True, ("small table", small_min, I, w))
+
+
 def test_global_hash_path_matches_oracle(ctx, oracle):
     # bound = min(n, E + I*w*dg) > 16384 -> the visited hash lives in global memory
     n, dim = 20000, 8
