@@ -316,10 +316,24 @@ def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, i
                              np.array_equal(d_counts.cpu().numpy().view(np.uint32), cnt_ref))],
                         dtype=torch.int32, device=dev)
     dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    st = ctx.last_search_stats() if args.exchange != "fused" else None
     ctx.close()
     ms = float(t[0])
+    xch = None
+    if st and st["units"]:
+        # bulk protocol, per GPU and step: every remote candidate costs an 8 B
+        # request out and an 8 B key back (a uniform id-range shard makes
+        # (R-1)/R of the visited vectors remote), each query is copied once to
+        # every other rank; HBM side: the same algorithmic bytes as K1
+        vis_q = st["visited"] / st["units"]
+        xbytes = nq * (vis_q * (world - 1) / world * 16 + (world - 1) * 4 * dim)
+        alg = nq * (vis_q * 4 * dim + st["expanded"] / st["units"] * 4 * args.degree + 4 * dim)
+        step_s = ms / args.steps / 1e3
+        xch = {"bytes_per_step_per_gpu": xbytes, "achieved_gbs": xbytes / step_s / 1e9,
+               "nvlink_peak_gbs_per_direction": 900.0, "frac": xbytes / step_s / 1e9 / 900.0,
+               "hbm_alg_gbs_per_gpu": alg / step_s / 1e9, "visited_per_query": vis_q}
     return {"value": nq * world * args.steps / (ms / 1e3), "unit": "queries/s",
-            "ms_per_step": ms / args.steps,
+            "ms_per_step": ms / args.steps, "exchange_roofline": xch,
             "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; " + (
                 "bulk-synchronous NVLink peer-store frontier exchange (xchg_kernel.cu)" if args.exchange == "bulk"
                 else "bulk protocol, host-driven ncclSend/ncclRecv exchange (baseline)" if args.exchange == "nccl"
