@@ -34,6 +34,12 @@
 namespace dvsg {
 namespace {
 
+#ifndef DVSG_K1_GLOBAL_PTX
+#define DVSG_K1_GLOBAL_PTX 0  // measured: explicit ld.global/atom.global probes -0.3%
+#endif
+#ifndef DVSG_K1_BATCH_PROBES
+#define DVSG_K1_BATCH_PROBES 0  // measured: batched probe rounds -4%
+#endif
 #ifndef DVSG_K1_SORT_RUNS
 #define DVSG_K1_SORT_RUNS 0
 #endif
@@ -58,6 +64,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   uint64_t* surv = pool_alt + a.cap;
   uint32_t* cand = reinterpret_cast<uint32_t*>(surv + a.chp);
   uint32_t* frontier = cand + kChunk;
+  const bool gtab = a.hash_global != nullptr;
   uint32_t* const region = a.hash_global ? a.hash_global + (size_t)blockIdx.x * (size_t)(a.hsize + a.hsmall)
                                          : frontier + ((a.beam + 3) & ~3);
   const uint32_t dg_magic = (uint32_t)((0x100000000ull + (uint64_t)a.dg - 1) / (uint64_t)a.dg);
@@ -192,10 +199,51 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           }
         }
         __syncthreads();  // st.ncand reset visible
+#if DVSG_K1_BATCH_PROBES
+        // global table: every probe round issues the loads of all 8 ids, then
+        // their CASes, before using a result (an empty slot is always CASed,
+        // so afterwards cur == kEmpty means "claimed")
+        unsigned fresh = 0;
+        if (gtab) {
+          uint32_t hs[kRawPerThread];
+          unsigned pend = 0;
+#pragma unroll
+          for (int j = 0; j < kRawPerThread; ++j) {
+            hs[j] = (hash_slot(ids[j]) >> 7) & hmask;
+            if (ids[j] != kEmpty) pend |= 1u << j;
+          }
+          while (pend) {
+            uint32_t cur[kRawPerThread];
+#pragma unroll
+            for (int j = 0; j < kRawPerThread; ++j) cur[j] = (pend >> j) & 1u ? ld_global_u32(table + hs[j]) : 0u;
+#pragma unroll
+            for (int j = 0; j < kRawPerThread; ++j)
+              if (((pend >> j) & 1u) && cur[j] == kEmpty) cur[j] = cas_global_u32(table + hs[j], kEmpty, ids[j]);
+#pragma unroll
+            for (int j = 0; j < kRawPerThread; ++j) {
+              if (!((pend >> j) & 1u)) continue;
+              if (cur[j] == kEmpty) {
+                fresh |= 1u << j;
+                pend &= ~(1u << j);
+              } else if (cur[j] == ids[j]) {
+                pend &= ~(1u << j);
+              } else {
+                hs[j] = (hs[j] + 1u) & hmask;
+              }
+            }
+          }
+        }
+#endif
 #pragma unroll
         for (int j = 0; j < kRawPerThread; ++j) {
           if (j * kThreads >= rcount) break;  // block-uniform
-          const bool isnew = ids[j] != kEmpty && visit_insert(table, hmask, ids[j]);
+#if DVSG_K1_BATCH_PROBES
+          const bool isnew = gtab ? ((fresh >> j) & 1u) != 0
+                                  : (ids[j] != kEmpty && visit_insert(table, hmask, ids[j]));
+#else
+          const bool isnew = ids[j] != kEmpty && ((DVSG_K1_GLOBAL_PTX && gtab) ? visit_insert_global(table, hmask, ids[j])
+                                                                             : visit_insert(table, hmask, ids[j]));
+#endif
           const unsigned bal = __ballot_sync(full, isnew);
           int base = 0;
           if (lane == 0 && bal) base = atomicAdd(&st.ncand, __popc(bal));
