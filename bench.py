@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["dvsg", "reference"], default="dvsg")
-    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=1_000_000)
     ap.add_argument("--nq", type=int, default=100_000)
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--rank-latent", type=int, default=16)
