@@ -279,6 +279,15 @@ def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, i
     from paper_2512_02278_b200.dist import prepare_step, setup_sharded
     g0 = index.graphs[0]
     ctx = dvs.Context(local)
+    try:
+        return _measure_sharded(ctx, args, torch, dist, rank, world, data, queries, g0, p, ids_ref,
+                                cnt_ref, flush, dev, setup_sharded, prepare_step)
+    finally:
+        ctx.close()
+
+
+def _measure_sharded(ctx, args, torch, dist, rank, world, data, queries, g0, p, ids_ref, cnt_ref, flush,
+                     dev, setup_sharded, prepare_step):
     ctx.set_shard_exchange(args.exchange)
     setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
     if args.exchange == "nccl":
@@ -317,7 +326,6 @@ def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, i
                         dtype=torch.int32, device=dev)
     dist.all_reduce(same, op=dist.ReduceOp.MIN)
     st = ctx.last_search_stats() if args.exchange != "fused" else None
-    ctx.close()
     ms = float(t[0])
     xch = None
     if st and st["units"]:
@@ -535,9 +543,14 @@ def main():
     # ---- node-sharded mode beside the replica headline (N > 1) -------------------------
     sharded_side = None
     if world > 1 and not sharded and args.mode == "auto":
-        sharded_side = measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries,
-                                       index, p, ids_h, cnt_h, flush, dev)
-        if args.exchange != "nccl" and not args.no_nccl_baseline:
+        # side measurements must not cost the headline line: a failure (raised
+        # on every rank alike, e.g. out of memory) is reported in the JSON
+        try:
+            sharded_side = measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries,
+                                           index, p, ids_h, cnt_h, flush, dev)
+        except Exception as e:  # noqa: BLE001
+            sharded_side = {"error": f"{type(e).__name__}: {e}"}
+        if "error" not in sharded_side and args.exchange != "nccl" and not args.no_nccl_baseline:
             # the same protocol over host-driven NCCL send/recv: the measured baseline
             ex = args.exchange
             args.exchange = "nccl"
@@ -545,6 +558,8 @@ def main():
                 sharded_side["nccl_baseline"] = measure_sharded(
                     args, dvs, torch, dist, local, rank, world, data, queries, index, p, ids_h, cnt_h,
                     flush, dev)
+            except Exception as e:  # noqa: BLE001
+                sharded_side["nccl_baseline"] = {"error": f"{type(e).__name__}: {e}"}
             finally:
                 args.exchange = ex
 
