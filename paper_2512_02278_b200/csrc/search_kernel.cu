@@ -34,6 +34,9 @@
 namespace dvsg {
 namespace {
 
+#ifndef DVSG_K1_CHUNK_FILTER
+#define DVSG_K1_CHUNK_FILTER 0  // measured: within-chunk smem duplicate filter -12%
+#endif
 #ifndef DVSG_K1_GLOBAL_PTX
 #define DVSG_K1_GLOBAL_PTX 0  // measured: explicit ld.global/atom.global probes -0.3%
 #endif
@@ -177,6 +180,14 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           st.ncand = 0;
           st.nsurv = 0;
         }
+#if DVSG_K1_CHUNK_FILTER
+        // within-chunk duplicate filter in the (idle until scoring) survivor
+        // buffer: only an id's first occurrence in the chunk probes the
+        // visited table (exact: a filtered id is a repeat of a probed one)
+        uint32_t* const filt = reinterpret_cast<uint32_t*>(surv);
+        constexpr int kFilt = 2 * kChunk;  // u32 slots (surv holds >= kChunk u64)
+        for (int i = tid; i < kFilt; i += kThreads) filt[i] = kEmpty;
+#endif
         // ---- gather raw ids (all loads first for MLP), then dedup
         uint32_t ids[kRawPerThread];
 #pragma unroll
@@ -241,8 +252,24 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           const bool isnew = gtab ? ((fresh >> j) & 1u) != 0
                                   : (ids[j] != kEmpty && visit_insert(table, hmask, ids[j]));
 #else
-          const bool isnew = ids[j] != kEmpty && ((DVSG_K1_GLOBAL_PTX && gtab) ? visit_insert_global(table, hmask, ids[j])
-                                                                             : visit_insert(table, hmask, ids[j]));
+          bool first = ids[j] != kEmpty;
+#if DVSG_K1_CHUNK_FILTER
+          if (first) {
+            uint32_t h = (ids[j] * 0x85EBCA6Bu >> 19) & (kFilt - 1);
+#pragma unroll 1
+            for (int t = 0; t < 8; ++t) {  // bounded: an unresolved id just probes the table
+              const uint32_t cur = atomicCAS(filt + h, kEmpty, ids[j]);
+              if (cur == kEmpty) break;
+              if (cur == ids[j]) {
+                first = false;
+                break;
+              }
+              h = (h + 1) & (kFilt - 1);
+            }
+          }
+#endif
+          const bool isnew = first && ((DVSG_K1_GLOBAL_PTX && gtab) ? visit_insert_global(table, hmask, ids[j])
+                                                                   : visit_insert(table, hmask, ids[j]));
 #endif
           const unsigned bal = __ballot_sync(full, isnew);
           int base = 0;
