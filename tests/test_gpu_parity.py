@@ -318,12 +318,23 @@ def test_device_entry_points_and_distributed_pipeline_single_rank(ctx, golden):
     ctx.assign_top_c_device(d_q.data_ptr(), len(q), q.shape[1], 3, out.data_ptr())
     ctx.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint32), ctx.assign_top_c(q, 3))
-    if not dist.is_initialized():
+    own_pg = not dist.is_initialized()
+    if own_pg:
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
             port = s.getsockname()[1]
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                                 device_id=dev)
+    try:
+        _distributed_pipeline_checks(ctx, res, q, d_q, dev)
+    finally:
+        if own_pg:
+            dist.destroy_process_group()
+
+
+def _distributed_pipeline_checks(ctx, res, q, d_q, dev):
+    import torch
+    from paper_2512_02278_b200.dist import run_pipeline_distributed
     placement = torch.zeros(8, dtype=torch.int64, device=dev)
     for fo in (1, 2, 3):
         ids, dists, counts, vecs, vt = run_pipeline_distributed(ctx, d_q, dvs.SearchParams(6, 16, 10, 16), fo,
@@ -404,6 +415,44 @@ def test_sharded_bulk_waves_and_shapes(ctx, oracle, monkeypatch):
         want = ctx.beam_search(0, q, p)
         got = ctx.beam_search_sharded_emulated(R, q, p)
         _assert_same(got, want, True, ("bulk waves", n, dim, R, metric))
+
+
+@pytest.mark.parametrize("exchange", ["bulk", "fused", "nccl"])
+def test_sharded_multi_gpu_api_single_rank(oracle, exchange):
+    """The real multi-GPU entry points (shard_init / IPC export + connect /
+    NCCL connect / prepare / search_sharded_device) at one rank: every code
+    path of the device-side exchange runs, results equal the reference."""
+    import torch
+    n, dim = 2500, 24
+    v = sift_like(n, dim, 6, 501)
+    adj = oracle.build_graph(v, 16)
+    eo = oracle.compute_entry_order(v)
+    q = sift_like(70, dim, 6, 502)
+    gids = np.arange(n, dtype=np.uint32)
+    I, w, k, E = 5, 24, 10, 24
+    want = oracle.beam_search(v, gids, adj, eo, q, I, w, k, E)
+    cx = dvs.Context(0)
+    try:
+        cx.set_shard_exchange(exchange)
+        cx.shard_init(1, 0, v, n, adj, eo)
+        cx.shard_connect([cx.shard_export()])
+        if exchange == "nccl":
+            cx.nccl_connect(cx.nccl_unique_id())
+        cx.shard_prepare()
+        dev = torch.device("cuda", 0)
+        d_q = torch.from_numpy(q).to(dev)
+        ids = torch.empty((len(q), k), dtype=torch.int32, device=dev)
+        dists = torch.empty((len(q), k), dtype=torch.float32, device=dev)
+        cnt = torch.empty((len(q),), dtype=torch.int32, device=dev)
+        vis = torch.empty((len(q),), dtype=torch.int64, device=dev)
+        cx.search_sharded_device(d_q.data_ptr(), len(q), dim, dvs.SearchParams(I, w, k, E, accum="f32"),
+                                 ids.data_ptr(), dists.data_ptr(), cnt.data_ptr(), vis.data_ptr())
+        cx.synchronize()
+        got = (ids.cpu().numpy().view(np.uint32), dists.cpu().numpy(), cnt.cpu().numpy().view(np.uint32),
+               vis.cpu().numpy().view(np.uint64))
+        _assert_same(got, want, True, exchange)
+    finally:
+        cx.close()
 
 
 def test_sharded_emulated_golden(ctx, golden):
