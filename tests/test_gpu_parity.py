@@ -401,6 +401,7 @@ def test_sharded_bulk_waves_and_shapes(ctx, oracle, monkeypatch):
     ragged rank split, tiny partition (entry_count > n), IP metric, f64."""
     monkeypatch.setenv("DVSG_XG_WAVE", "7")
     for (n, dim, nq, R, w, k, E, metric, accum) in [(2500, 37, 61, 3, 16, 10, 16, "l2", "f32"),
+                                                      (900, 12, 3, 8, 8, 5, 8, "l2", "f32"),  # ranks without queries
                                                       (40, 8, 23, 4, 8, 20, 64, "l2", "f64"),
                                                       (1800, 24, 50, 2, 32, 5, 32, "ip", "f32")]:
         v = sift_like(n, dim, 6, 301 + n)
