@@ -9,31 +9,35 @@
 //
 // Instead of a per-CTA request/reply round trip (shard_kernel.cu, latency
 // bound: ~40 us per trip, 7 trips per query), every query of the wave advances
-// one phase at a time, and each phase is two bandwidth-bound kernels:
+// one phase at a time; per phase there are two kinds of work:
 //
-//   xg_expand (origin, CTA per query):
+//   origin (expand_unit, CTA per query):
 //     merge the keys the owners returned for the previous phase into the pool
-//     (exact cap-th-key filter, bitonic sort, merge path -- as K1), pick the
-//     frontier (first w unexpanded, graph_index.cpp:156-161), gather its
-//     adjacency rows, dedup against the visited hash (exact, per query in
-//     HBM), bucket the new ids by owner, reserve a contiguous inbox range at
-//     each owner (one peer atomic per owner) and write the requests there with
+//     (exact threshold filter, sort, merge path -- as K1), pick the frontier
+//     (first w unexpanded, graph_index.cpp:156-161), gather its adjacency
+//     rows, dedup against the visited hash (exact, per query in HBM), bucket
+//     the new ids by owner, reserve a contiguous inbox range at each owner
+//     (one peer atomic per owner) and write the requests there with
 //     coalesced NVLink peer stores;
-//   -- peer-flag barrier --
-//   xg_score (owner, warp per 32 requests):
-//     gather the rows (float4, 8 in flight per warp), score them exactly as K1
-//     (same lane partials and butterfly tree, so the same bits), and store the
-//     32 keys with one coalesced peer store into the origin's reply range
+//   -- peer-flag barrier (xg_barrier) --
+//   owner (score_warp_block, warp per 32 requests):
+//     gather the rows (float4, 8 in flight per warp), score them exactly as
+//     K1 (same lane partials and butterfly tree, so the same bits), and store
+//     the 32 keys with one coalesced peer store into the origin's reply range
 //     (same index as the inbox slot, so the origin needs no ids back);
 //   -- peer-flag barrier --
 //
-// Phase 0 expands the entry nodes, phases 1..I the frontiers, and a last
-// xg_expand pass (phase I+1) merges the final replies and writes the
+// Two lanes (query waves) run half a phase apart and every xg_step launch
+// carries one lane's origin items and the other lane's owner blocks, CTAs
+// split by role, so latency-bound origin work and HBM-bound gathers share the
+// SMs.  Phase 0 expands the entry nodes, phases 1..I the frontiers, and a
+// last origin pass (phase I+1) merges the final replies and writes the
 // (dist, gid)-sorted top-k (graph_index.cpp:173-186).  Traffic per remote
 // candidate: 8 B request + 8 B key over NVLink instead of a 4*d-byte gather;
 // load balance across ranks follows the (uniform) shard rule, not the query
 // split.  Emulation (all ranks on one device) runs the same kernels with the
-// barrier replaced by stream order.
+// barrier replaced by stream order; the NCCL baseline runs them over local
+// slabs with host-driven ncclSend/ncclRecv in place of the peer stores.
 #include <cstdint>
 #include <cuda_runtime.h>
 
