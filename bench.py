@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--mode", choices=["auto", "replica", "sharded"], default="auto",
                     help="N>1 layout: full index per GPU, or node-sharded vectors with an NVLink "
                          "frontier exchange (auto = replica headline, sharded measured beside it)")
+    ap.add_argument("--timeline-out", default=None,
+                    help="write the measured e2e pipeline timeline (intervals JSON) here")
     ap.add_argument("--no-nccl-baseline", action="store_true",
                     help="skip the NCCL-exchange baseline measured beside the sharded mode at N>1")
     ap.add_argument("--exchange", choices=["bulk", "fused", "nccl"], default="bulk",
@@ -251,6 +253,34 @@ def run_reference_impl(args, world, rank):
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def timeline_summary(dvs, tl, args):
+    """Measured copy/compute timeline of the last e2e step:
+    validated with check_timeline (simulator.cpp:170-217 rules), with the
+    time both lanes were busy (the overlap the microbatch pipeline buys)."""
+    if not tl:
+        return None
+    if getattr(args, "timeline_out", None):
+        with open(args.timeline_out, "w") as f:
+            json.dump(tl, f, indent=1)
+
+    def union(ivs):
+        out = []
+        for a, b in sorted((iv["start"], iv["end"]) for iv in ivs):
+            if out and a <= out[-1][1]:
+                out[-1][1] = max(out[-1][1], b)
+            else:
+                out.append([a, b])
+        return out
+
+    comp = union([iv for iv in tl if iv["lane"] == "compute"])
+    comm = union([iv for iv in tl if iv["lane"] == "comm"])
+    both = sum(max(0.0, min(b1, b2) - max(a1, a2)) for a1, b1 in comp for a2, b2 in comm)
+    return {"microbatches": 1 + max(iv["microbatch"] for iv in tl), "check_timeline": dvs.check_timeline(tl) or "ok",
+            "makespan_ms": max(iv["end"] for iv in tl), "compute_busy_ms": sum(b - a for a, b in comp),
+            "copy_busy_ms": sum(b - a for a, b in comm), "overlapped_ms": both,
+            "lanes": "comm = h2d + d2h on the copy stream, compute = run_pipeline kernels"}
 
 
 def workload_config(args, world, rec):
@@ -538,7 +568,8 @@ def main():
         d2h = out["ids"].nbytes + out["dists"].nbytes + out["counts"].nbytes + out["vectors"].nbytes + 4 + 8
         e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": float(e_ms[0]) / args.steps}
+               "ms_per_step": float(e_ms[0]) / args.steps,
+               "timeline": timeline_summary(dvs, ctx.last_pipeline_timeline(rank), args)}
 
     # ---- node-sharded mode beside the replica headline (N > 1) -------------------------
     sharded_side = None

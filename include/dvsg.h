@@ -247,6 +247,13 @@ dvsg_status dvsg_brute_force_topk(dvsg_ctx *ctx, const float *db, uint64_t n, in
  * last pipeline call, measured with CUDA events on the compute stream;
  * enable with dvsg_set_timing(ctx, 1). */
 dvsg_status dvsg_set_timing(dvsg_ctx *ctx, int enabled);
+/* Measured timeline of the last dvsg_run_pipeline with timing on (SURVEY
+ * 8f-4; the reference models one in replay_schedule, simulator.cpp:71-168):
+ * per microbatch 6 times in ms from the pipeline start -- H2D start/end
+ * (copy stream), compute start/end (compute stream: finiteness check,
+ * assign, route, K1, combine, hit vectors), D2H start/end (copy stream).
+ * out holds 6 x max_microbatches doubles; *n_out = microbatches written. */
+dvsg_status dvsg_last_pipeline_timeline(dvsg_ctx *ctx, double *out, int max_microbatches, int *n_out);
 dvsg_status dvsg_last_timings(dvsg_ctx *ctx, float *search_ms, float *assign_ms,
                               float *combine_ms, float *total_ms);
 /* Number of library kernels launched by this context since creation. */

@@ -237,6 +237,8 @@ class Ref:
         L.dvsref_compute_entry_order.argtypes = [c_void_p, c_uint64, c_int, c_void_p]
         L.dvsref_beam_search.argtypes = [c_void_p, c_void_p, c_uint64, c_int, c_int, c_int, c_int,
                                          c_int, c_void_p, c_void_p, c_void_p, c_void_p]
+        L.dvsref_check_timeline.argtypes = [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                            c_void_p, c_char_p, c_int]
         L.dvsref_combine_results.argtypes = [c_int, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                              c_void_p, c_void_p, c_void_p]
         L.dvsref_assign_top_c.argtypes = [c_void_p, c_int, c_int, c_void_p, c_uint64, c_int, c_void_p]
@@ -278,6 +280,20 @@ class Ref:
         eo = np.zeros(n, np.uint32)
         self.lib.dvsref_graph_arrays(h, _p(adj), _p(eo), None)
         return RefGraph(self, h, v.shape[1]), adj, eo
+
+    def check_timeline(self, intervals):
+        """simulator.cpp:170-217 on intervals with the reference's lane /
+        stage names -> None or the reference's message."""
+        lanes = {"compute": 0, "comm": 1}
+        stages = {"kmeans": 0, "dispatch": 1, "search": 2, "combine": 3}
+        n = len(intervals)
+        cols = [np.array([f(iv) for iv in intervals], dt) for f, dt in (
+            (lambda iv: iv["rank"], np.int32), (lambda iv: lanes[iv["lane"]], np.int32),
+            (lambda iv: stages[iv["stage"]], np.int32), (lambda iv: iv["microbatch"], np.int32),
+            (lambda iv: iv["start"], np.float64), (lambda iv: iv["end"], np.float64))]
+        msg = ctypes.create_string_buffer(512)
+        r = self.lib.dvsref_check_timeline(n, *[_p(c) for c in cols], msg, 512)
+        return None if r == 0 else msg.value.decode()
 
     def graph_from_arrays(self, v, gids, adjacency):
         v = np.ascontiguousarray(v, np.float32)

@@ -8,6 +8,7 @@
 // restatement in dvs_oracle.c, (b) generate tests/golden/ fixtures, and
 // (c) serve as the "reference" CPU baseline in bench.py.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -184,6 +185,20 @@ int dvsref_combine_results(int nparts, const std::uint32_t* ids, const float* di
     }
     *out_count = static_cast<std::uint32_t>(out.size());
   });
+}
+
+// check_timeline, simulator.cpp:170-217.  Returns 0 when valid, 1 with the
+// reference's message in msg (truncated to cap) otherwise.
+int dvsref_check_timeline(int n, const int* rank, const int* lane, const int* stage, const int* mb,
+                          const double* start, const double* end, char* msg, int cap) {
+  dvs::Timeline tl;
+  for (int i = 0; i < n; ++i)
+    tl.intervals.push_back({rank[i], static_cast<dvs::Lane>(lane[i]), static_cast<dvs::Stage>(stage[i]),
+                            mb[i], start[i], end[i]});
+  const auto r = dvs::check_timeline(tl);
+  if (!r) return 0;
+  std::snprintf(msg, static_cast<std::size_t>(cap), "%s", r->c_str());
+  return 1;
 }
 
 // assign_top_c, kmeans.cpp:243-280

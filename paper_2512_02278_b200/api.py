@@ -41,7 +41,7 @@ __all__ = [
     "Context", "default_context", "beam_search_stats", "beam_search", "visited_count",
     "beam_search_batch", "compute_entry_order", "build_graph", "combine_results",
     "assign_top_c", "place_clusters", "route", "run_pipeline", "load_index", "save_index",
-    "InvalidArgument", "FormatError", "InternalError",
+    "check_timeline", "InvalidArgument", "FormatError", "InternalError",
 ]
 
 
@@ -428,6 +428,65 @@ class Context:
         check(lib.dvsg_last_timings(self._h, *[ctypes.byref(v) for v in vals]))
         return {"search_ms": vals[0].value, "assign_ms": vals[1].value,
                 "combine_ms": vals[2].value, "total_ms": vals[3].value}
+
+    def last_pipeline_timeline(self, rank: int = 0) -> List[dict]:
+        """Measured intervals of the last run_pipeline made with timing on:
+        per microbatch h2d (comm lane), search (compute lane), d2h (comm
+        lane), ms from the pipeline start -- the measured counterpart of the
+        reference's modeled Timeline (simulator.hpp Interval fields)."""
+        buf = np.zeros(6 * 16, np.float64)
+        n = ctypes.c_int(0)
+        check(lib.dvsg_last_pipeline_timeline(self._h, _ptr(buf), 16, ctypes.byref(n)))
+        out = []
+        for mb in range(n.value):
+            t = buf[6 * mb:6 * mb + 6]
+            for stage, lane, a, b in (("h2d", "comm", t[0], t[1]), ("search", "compute", t[2], t[3]),
+                                      ("d2h", "comm", t[4], t[5])):
+                out.append({"rank": rank, "lane": lane, "stage": stage, "microbatch": mb,
+                            "start": float(a), "end": float(b)})
+        return out
+
+
+TIMELINE_STAGE_ORDER = {"kmeans": 0, "dispatch": 1, "search": 2, "combine": 3}
+MEASURED_STAGE_ORDER = {"h2d": 0, "search": 1, "d2h": 2}
+
+
+def check_timeline(intervals, stage_order=None) -> Optional[str]:
+    """check_timeline, simulator.cpp:170-217: no two intervals of one (rank,
+    lane) overlap, and every stage of a (rank, microbatch) starts after its
+    predecessor ends.  Returns None or the reference's error message.
+    stage_order defaults to the measured pipeline's (h2d, search, d2h) when
+    the intervals use those names, else the reference's four stages."""
+    if stage_order is None:
+        stage_order = MEASURED_STAGE_ORDER if any(iv["stage"] in MEASURED_STAGE_ORDER and iv["stage"] != "search"
+                                                  for iv in intervals) else TIMELINE_STAGE_ORDER
+    lanes = {}
+    for iv in intervals:
+        if iv["end"] < iv["start"]:
+            return f"interval with end < start on rank {iv['rank']}"
+        lanes.setdefault((iv["rank"], iv["lane"]), []).append(iv)
+    lane_order = {"compute": 0, "comm": 1}
+    for (rank, lane) in sorted(lanes, key=lambda kv: (kv[0], lane_order.get(kv[1], 2))):
+        ivs = sorted(lanes[(rank, lane)], key=lambda v: (v["start"], v["end"]))
+        for a, b in zip(ivs, ivs[1:]):
+            if b["start"] < a["end"]:
+                return f"overlap on rank {rank} lane {lane} at t={b['start']:.6f}"
+    by_stage = {}
+    for iv in intervals:
+        key = (iv["rank"], iv["microbatch"], stage_order[iv["stage"]])
+        if key in by_stage:
+            return f"duplicate stage interval for rank {iv['rank']} microbatch {iv['microbatch']}"
+        by_stage[key] = iv
+    for (rank, mb, s), iv in sorted(by_stage.items()):
+        if s == 0:
+            continue
+        prev = by_stage.get((rank, mb, s - 1))
+        if prev is None:
+            return f"missing predecessor stage for rank {rank} microbatch {mb}"
+        if iv["start"] < prev["end"]:
+            return (f"dependency violation: {iv['stage']} of microbatch {mb} starts before "
+                    f"{prev['stage']} ends")
+    return None
 
 
 _default: Optional[Context] = None

@@ -201,6 +201,10 @@ struct dvsg_ctx {
   bool timing = false;
   cudaEvent_t ev[8] = {};
   cudaEvent_t mb_ev[2 * 16] = {};  // microbatch pipeline (H2D done, compute done)
+  // measured timeline of the last run_pipeline (timing on): base + per
+  // microbatch {h2d start, h2d end, compute start, compute end, d2h start, d2h end}
+  cudaEvent_t tl_ev[1 + 6 * 16] = {};
+  int tl_mb = 0;
   float t_search = 0, t_assign = 0, t_combine = 0, t_total = 0;
   int timing_pending = 0;  // 1: search only, 2: pipeline
   std::atomic<uint64_t> launches{0};
@@ -1124,6 +1128,7 @@ dvsg_status dvsg_create(int device, dvsg_ctx** out) {
 
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
     for (auto& e : c->mb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : c->tl_ev) cuda_check(cudaEventCreate(&e), "event");
     *out = c.release();
   });
 }
@@ -1139,6 +1144,7 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     if (c->nccl) nccl_api().comm_destroy(c->nccl);
     for (auto& e : c->ev) cudaEventDestroy(e);
     for (auto& e : c->mb_ev) cudaEventDestroy(e);
+    for (auto& e : c->tl_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm);
 
@@ -1634,20 +1640,32 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
       const uint64_t w = taper ? i * mb - i * (i - 1) / 2 : i;
       return nq * w / wsum;
     };
+    // measured timeline (timing on): 6 events per microbatch
+    const bool tl = c->timing;
+    cudaEvent_t* tv = c->tl_ev + 1;
+    c->tl_mb = tl ? (int)mb : 0;
+    if (tl) cuda_check(cudaEventRecord(c->tl_ev[0], xs), "event");
     // every H2D first: a D2H queued on the copy stream waits for its batch's
     // compute, so an H2D queued behind it would serialize the whole pipeline
     for (uint64_t i = 0; i < mb; ++i) {
       const uint64_t q0 = edge(i), n_i = edge(i + 1) - q0;
-      if (n_i == 0) continue;
-      cuda_check(cudaMemcpyAsync(c->io_f.p + q0 * (uint64_t)dim, queries + q0 * (uint64_t)dim,
-                                 n_i * (uint64_t)dim * 4, cudaMemcpyHostToDevice, xs), "H2D");
+      if (tl) cuda_check(cudaEventRecord(tv[6 * i + 0], xs), "event");
+      if (n_i)
+        cuda_check(cudaMemcpyAsync(c->io_f.p + q0 * (uint64_t)dim, queries + q0 * (uint64_t)dim,
+                                   n_i * (uint64_t)dim * 4, cudaMemcpyHostToDevice, xs), "H2D");
+      if (tl) cuda_check(cudaEventRecord(tv[6 * i + 1], xs), "event");
       cuda_check(cudaEventRecord(evh[i], xs), "event");
     }
     for (uint64_t i = 0; i < mb; ++i) {
       const uint64_t q0 = edge(i), q1 = edge(i + 1), n_i = q1 - q0;
-      if (n_i == 0) continue;
+      if (n_i == 0) {
+        if (tl)
+          for (int e = 2; e < 6; ++e) cuda_check(cudaEventRecord(tv[6 * i + e], xs), "event");
+        continue;
+      }
       float* dq = c->io_f.p + q0 * (uint64_t)dim;
       cuda_check(cudaStreamWaitEvent(cs, evh[i], 0), "wait");
+      if (tl) cuda_check(cudaEventRecord(tv[6 * i + 2], cs), "event");
       cuda_check(dvsg::launch_check_finite(dq, n_i * (uint64_t)dim, c->err_flag.p, cs), "finite check");
       c->launches += 1;
       uint32_t* ids_i = c->io_u.p + q0 * k;
@@ -1655,12 +1673,15 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
       float* d_i = od.p + q0 * k;
       float* v_i = out_vectors ? ov.p + q0 * k * (uint64_t)dim : nullptr;
       pipeline_device(c, dq, n_i, dim, p, fanout, ids_i, d_i, cnt_i, v_i, c->u_visited.p + q0 * (uint64_t)fanout, false);
+      if (tl) cuda_check(cudaEventRecord(tv[6 * i + 3], cs), "event");
       cuda_check(cudaEventRecord(evc[i], cs), "event");
       cuda_check(cudaStreamWaitEvent(xs, evc[i], 0), "wait");
+      if (tl) cuda_check(cudaEventRecord(tv[6 * i + 4], xs), "event");
       cuda_check(cudaMemcpyAsync(out_ids + q0 * k, ids_i, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
       cuda_check(cudaMemcpyAsync(out_dists + q0 * k, d_i, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
       cuda_check(cudaMemcpyAsync(out_count + q0, cnt_i, n_i * 4, cudaMemcpyDeviceToHost, xs), "D2H");
       if (out_vectors) cuda_check(cudaMemcpyAsync(out_vectors + q0 * k * (uint64_t)dim, v_i, n_i * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      if (tl) cuda_check(cudaEventRecord(tv[6 * i + 5], xs), "event");
     }
     cuda_check(dvsg::launch_reduce_u64(c->u_visited.p, nq * (uint64_t)fanout, reinterpret_cast<unsigned long long*>(c->io_u64.p), cs), "reduce");
     c->launches += 1;
@@ -1765,6 +1786,23 @@ dvsg_status dvsg_nccl_connect(dvsg_ctx* c, const void* id128) {
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof id);
     nccl_check(nccl_api().comm_init_rank(&c->nccl, c->sh.nranks, id, c->sh.rank), "ncclCommInitRank");
+  });
+}
+
+dvsg_status dvsg_last_pipeline_timeline(dvsg_ctx* c, double* out, int max_microbatches, int* n_out) {
+  return guarded([&] {
+    set_device(c);
+    *n_out = 0;
+    if (!c->tl_mb) return;
+    cuda_check(cudaEventSynchronize(c->tl_ev[6 * c->tl_mb]), "timeline");
+    const int m = std::min(c->tl_mb, max_microbatches);
+    for (int i = 0; i < m; ++i)
+      for (int e = 0; e < 6; ++e) {
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, c->tl_ev[0], c->tl_ev[1 + 6 * i + e]), "elapsed");
+        out[6 * i + e] = ms;
+      }
+    *n_out = m;
   });
 }
 

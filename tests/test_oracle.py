@@ -135,3 +135,30 @@ def test_kat_single_vector_partition(oracle):
     ids, d, c, vis = oracle.beam_search(v, np.array([42], np.uint32), adj, np.array([0], np.uint32),
                                         np.zeros((1, 3), np.float32), 2, 2, 5, 1)
     assert c[0] == 1 and ids[0, 0] == 42 and vis[0] == 1
+
+
+def test_check_timeline_matches_reference(ref):
+    """api.check_timeline restates simulator.cpp:170-217; pinned against the
+    reference's own check_timeline on random (often invalid) timelines."""
+    from paper_2512_02278_b200.api import check_timeline
+    rng = np.random.default_rng(11)
+    stages = ["kmeans", "dispatch", "search", "combine"]
+    lane_of = {"kmeans": "compute", "dispatch": "comm", "search": "compute", "combine": "comm"}
+    outcomes = set()
+    for case in range(400):
+        ivs = []
+        for mb in range(int(rng.integers(1, 4))):
+            t = float(rng.integers(0, 5))
+            for s in stages:
+                if rng.random() < 0.05:
+                    continue  # missing stage
+                d = float(rng.integers(-1, 4)) * 0.5
+                start = t + float(rng.integers(-2, 3)) * 0.5
+                ivs.append({"rank": int(rng.integers(0, 2)), "lane": lane_of[s], "stage": s,
+                            "microbatch": mb, "start": start, "end": start + d})
+                t = start + max(d, 0.0)
+        want = ref.check_timeline(ivs)
+        got = check_timeline(ivs, stage_order={s: i for i, s in enumerate(stages)})
+        assert got == want, (case, ivs)
+        outcomes.add(None if want is None else want.split()[0])
+    assert len(outcomes) >= 3  # valid and several failure kinds exercised
