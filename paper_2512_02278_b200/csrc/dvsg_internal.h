@@ -161,7 +161,7 @@ size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_sme
 constexpr int kChunk = 2048;  // raw candidates per dedup/score/merge chunk (8 per thread)
 
 // K5 assign (route_kernels.cu): nq x c cluster ids, exact fp64 expanded form.
-// scratch: nq x clusters u64 keys.
+// scratch: nq x (clusters + 1) u64 (keys + query norms of the tiled large-C path).
 cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const float* cents,
                           const double* cent_norms, int clusters, int c, uint32_t* out,
                           uint64_t* scratch, cudaStream_t stream);

@@ -997,7 +997,7 @@ void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const 
   c->err_flag.reserve(1, c->stream);
   if (reset_err) cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
-  c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
+  c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
   cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->assign_scratch.p, c->stream), "assign");
   cuda_check(dvsg::launch_route(c->assign.p, nq, fanout, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
@@ -1499,7 +1499,7 @@ dvsg_status dvsg_assign_top_c(dvsg_ctx* c, const float* queries, uint64_t nq, in
     if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
     const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
     c->assign.reserve(nq * (uint64_t)cc, c->stream);
-    c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
+    c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
     cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, c->assign.p, c->assign_scratch.p, c->stream), "assign");
     c->launches += 1;
     cuda_check(cudaMemcpyAsync(out, c->assign.p, nq * (uint64_t)cc * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
@@ -1515,7 +1515,7 @@ dvsg_status dvsg_assign_top_c_device(dvsg_ctx* c, const float* d_queries, uint64
     if (cc < 1 || cc > c->clusters) fail(DVSG_EINVAL, "assign_top_c: c=%d out of range for %d clusters", cc, c->clusters);
     if (dim != c->dim) fail(DVSG_EINVAL, "assign_top_c: query dim %d != centroid dim %d", dim, c->dim);
     if (nq == 0) return;
-    c->assign_scratch.reserve(nq * (uint64_t)c->clusters, c->stream);
+    c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
     cuda_check(dvsg::launch_assign(d_queries, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, d_out, c->assign_scratch.p, c->stream), "assign");
     c->launches += 1;
   });

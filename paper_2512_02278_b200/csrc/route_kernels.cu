@@ -1,9 +1,12 @@
 // route_kernels.cu -- K5 assign, route, K4 combine, hit-vector gather.
 //
 //   K5 assign   : assign_top_c, /root/reference/proj/src/kmeans.cpp:243-280.
-//                 One warp per query; each lane owns whole centroids and runs
-//                 the reference's own sequential fp64 dot / norm (kmeans.cpp
-//                 :44-48 expanded_dist), so the f32 distances are bit-exact.
+//                 The reference's own sequential fp64 dot / norm (kmeans.cpp
+//                 :44-48 expanded_dist), so the f32 distances are bit-exact:
+//                 C < 8: one warp per query, each lane owns whole centroids;
+//                 C >= 8: register-tiled 64 x 64 fp64 tiles (same per-output
+//                 accumulation order) + a per-lane top-c selection (SURVEY
+//                 8f-3; 12x faster at C = 4096).
 //   route       : router.cpp:52-79 -- one unit per (query, assigned cluster).
 //   K4 combine  : combine_results, simulator.cpp:219-243.  One warp per query
 //                 runs a <=32-way merge of the sorted partial lists on
@@ -11,6 +14,7 @@
 //                 unsorted partial (internal_error in the reference).
 //   gather      : simulator.cpp:329-333 -- attach the hit vectors.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "dvsg_internal.h"
@@ -70,6 +74,117 @@ __global__ void assign_kernel(const float* __restrict__ queries, uint64_t nq, in
     best = warp_min_u64(best);
     if (lane == 0) out[q * (uint64_t)c + r] = (uint32_t)best;
     last = best;
+  }
+}
+
+// ---- K5 at large C: register-tiled fp64 "GEMM" with the reference's order --
+// 64 queries x 64 centroids per CTA, 4 x 4 outputs per thread, k-chunks of
+// 16 staged in smem as fp64.  Every output still accumulates its dot product
+// over i = 0..dim-1 in order with separate round-to-nearest multiply and add
+// (distance.cpp:35-42 as compiled for x86-64: no contraction), so the keys
+// are bit-identical to assign_kernel's; only the data movement changes
+// (coalesced tiles instead of 32 strided centroid rows per warp).
+constexpr int kAT = 64, kAK = 16;
+
+__global__ void qnorm_kernel(const float* __restrict__ queries, uint64_t nq, int dim,
+                             double* __restrict__ qn) {
+  const uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const float* qp = queries + q * (uint64_t)dim;
+  double s = 0.0;  // squared_norm, distance.cpp:44-50 (sequential)
+  for (int i = 0; i < dim; ++i) s = __dadd_rn(s, __dmul_rn((double)qp[i], (double)qp[i]));
+  qn[q] = s;
+}
+
+__global__ void __launch_bounds__(256) assign_tile_kernel(const float* __restrict__ queries, uint64_t nq,
+                                                          int dim, const float* __restrict__ cents,
+                                                          const double* __restrict__ cent_norms,
+                                                          int clusters, const double* __restrict__ qn,
+                                                          uint64_t* __restrict__ scratch) {
+  __shared__ double qs[kAK][kAT];
+  __shared__ double cs[kAK][kAT];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const uint64_t q0 = (uint64_t)blockIdx.y * kAT;
+  const int c0 = blockIdx.x * kAT;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int k0 = 0; k0 < dim; k0 += kAK) {
+    // 64 rows x 16 dims of each operand: thread loads 4 elements of each
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + r * 256;  // 0..1023
+      const int row = e >> 4, kk = e & 15;
+      const int k = k0 + kk;
+      const uint64_t q = q0 + row;
+      qs[kk][row] = (q < nq && k < dim) ? (double)queries[q * (uint64_t)dim + k] : 0.0;
+      const int cc = c0 + row;
+      cs[kk][row] = (cc < clusters && k < dim) ? (double)cents[(uint64_t)cc * (uint64_t)dim + k] : 0.0;
+    }
+    __syncthreads();
+    const int kn = dim - k0 < kAK ? dim - k0 : kAK;
+    for (int kk = 0; kk < kn; ++kk) {
+      double qv[4], cv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qv[i] = qs[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cv[j] = cs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(qv[i], cv[j]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint64_t q = q0 + ty * 4 + i;
+    if (q >= nq) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cc = c0 + tx * 4 + j;
+      if (cc >= clusters) continue;
+      const double d = __dsub_rn(__dadd_rn(qn[q], cent_norms[cc]), __dmul_rn(2.0, acc[i][j]));
+      const float f = (float)(d < 0.0 ? 0.0 : d);
+      scratch[q * (uint64_t)clusters + cc] = ((uint64_t)f2ord(f) << 32) | (uint32_t)cc;
+    }
+  }
+}
+
+// top-c keys of each query row (c <= 32): per-lane sorted top-c in registers
+// over a strided pass, then c rounds of warp-min over the lane heads.
+template <int MC>
+__global__ void select_topc_kernel(const uint64_t* __restrict__ scratch, uint64_t nq, int clusters,
+                                   int c, uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t q = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const uint64_t* row = scratch + q * (uint64_t)clusters;
+  uint64_t top[MC];
+#pragma unroll
+  for (int r = 0; r < MC; ++r) top[r] = ~0ull;
+  for (int j = lane; j < clusters; j += 32) {
+    uint64_t key = row[j];
+    if (key >= top[MC - 1]) continue;  // keeps the lane's MC >= c smallest
+#pragma unroll
+    for (int r = 0; r < MC; ++r) {  // insertion: carry the larger key down
+      if (key < top[r]) {
+        const uint64_t t = top[r];
+        top[r] = key;
+        key = t;
+      }
+    }
+  }
+  for (int r = 0; r < c; ++r) {
+    const uint64_t best = warp_min_u64(top[0]);
+    if (lane == 0) out[q * (uint64_t)c + r] = (uint32_t)best;
+    if (top[0] == best) {  // keys are unique (cluster id in the low bits): one owner pops
+#pragma unroll
+      for (int s = 0; s < MC - 1; ++s) top[s] = top[s + 1];
+      top[MC - 1] = ~0ull;
+    }
   }
 }
 
@@ -246,6 +361,23 @@ cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const floa
                           const double* cent_norms, int clusters, int c, uint32_t* out,
                           uint64_t* scratch, cudaStream_t stream) {
   if (nq == 0) return cudaSuccess;
+  static const int tiled_min = [] {
+    const char* e = std::getenv("DVSG_ASSIGN_TILED_MIN");
+    return e ? std::atoi(e) : 8;  // measured: tiled 9x faster already at C=64
+  }();
+  if (tiled_min > 0 && clusters >= tiled_min && c <= 32) {
+    // scratch holds nq x clusters keys + nq query norms (host reserves both)
+    double* qn = reinterpret_cast<double*>(scratch + nq * (uint64_t)clusters);
+    qnorm_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, stream>>>(queries, nq, dim, qn);
+    const dim3 grid((unsigned)((clusters + kAT - 1) / kAT), (unsigned)((nq + kAT - 1) / kAT));
+    assign_tile_kernel<<<grid, 256, 0, stream>>>(queries, nq, dim, cents, cent_norms, clusters, qn, scratch);
+    const unsigned g = (unsigned)((nq + 7) / 8);
+    if (c <= 4) select_topc_kernel<4><<<g, 256, 0, stream>>>(scratch, nq, clusters, c, out);
+    else if (c <= 8) select_topc_kernel<8><<<g, 256, 0, stream>>>(scratch, nq, clusters, c, out);
+    else if (c <= 16) select_topc_kernel<16><<<g, 256, 0, stream>>>(scratch, nq, clusters, c, out);
+    else select_topc_kernel<32><<<g, 256, 0, stream>>>(scratch, nq, clusters, c, out);
+    return cudaGetLastError();
+  }
   const int wpb = 4;
   assign_kernel<<<(unsigned)((nq + wpb - 1) / wpb), 32 * wpb, 0, stream>>>(
       queries, nq, dim, cents, cent_norms, clusters, c, scratch, out);

@@ -280,6 +280,20 @@ def test_assign_matches_reference(ctx, oracle, golden):
         dvs.assign_top_c(cents, np.array([[5, 0]], np.float32), 3, ctx=ctx)
 
 
+@pytest.mark.parametrize("clusters,dim,c", [(128, 8, 4), (300, 37, 9), (1000, 128, 32), (513, 96, 1)])
+def test_assign_large_c_tiled_matches_reference(ctx, oracle, clusters, dim, c):
+    """Large-C K5 (register-tiled fp64 with the reference's accumulation
+    order + per-lane top-c selection) equals assign_top_c, ties by lower id
+    (duplicated centroids force exact distance ties)."""
+    cents = oracle.random_dataset(clusters, dim, 400 + clusters, -100, 100)
+    cents[clusters // 2:clusters // 2 + 5] = cents[3]
+    q = oracle.random_dataset(333, dim, 500 + clusters, -100, 100)
+    q[7] = cents[3]
+    want = oracle.assign_top_c(cents, q, c)
+    got = dvs.assign_top_c(cents, q, c, ctx=ctx)
+    assert np.array_equal(got, want)
+
+
 def test_pipeline_matches_reference_golden(ctx, golden):
     from fnsy import G3_FNSY
     res = golden("g3_mixture.npz")
