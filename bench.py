@@ -356,6 +356,22 @@ def _measure_sharded(ctx, args, torch, dist, rank, world, data, queries, g0, p, 
                         dtype=torch.int32, device=dev)
     dist.all_reduce(same, op=dist.ReduceOp.MIN)
     st = ctx.last_search_stats() if args.exchange != "fused" else None
+    tl_sum = None
+    if args.exchange != "fused":
+        # one more (untimed) step with timing on: measured step-kernel vs
+        # barrier / NCCL-exchange intervals on the search stream
+        ctx.set_timing(True)
+        prepare_step(ctx, dist.barrier)
+        run()
+        ctx.synchronize()
+        tl = ctx.last_sharded_timeline(rank)
+        ctx.set_timing(False)
+        if tl:
+            span = max(iv["end"] for iv in tl) - min(iv["start"] for iv in tl)
+            comp = sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == "compute")
+            comm = sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == "comm")
+            tl_sum = {"rank": rank, "intervals": len(tl), "span_ms": span, "step_kernels_ms": comp,
+                      "barrier_or_exchange_ms": comm, "exchange_share": comm / span if span else None}
     ms = float(t[0])
     xch = None
     if st and st["units"]:
@@ -371,7 +387,7 @@ def _measure_sharded(ctx, args, torch, dist, rank, world, data, queries, g0, p, 
                "nvlink_peak_gbs_per_direction": 900.0, "frac": xbytes / step_s / 1e9 / 900.0,
                "hbm_alg_gbs_per_gpu": alg / step_s / 1e9, "visited_per_query": vis_q}
     return {"value": nq * world * args.steps / (ms / 1e3), "unit": "queries/s",
-            "ms_per_step": ms / args.steps, "exchange_roofline": xch,
+            "ms_per_step": ms / args.steps, "exchange_roofline": xch, "timeline_rank0": tl_sum,
             "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; " + (
                 "bulk-synchronous NVLink peer-store frontier exchange (xchg_kernel.cu)" if args.exchange == "bulk"
                 else "bulk protocol, host-driven ncclSend/ncclRecv exchange (baseline)" if args.exchange == "nccl"

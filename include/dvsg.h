@@ -254,6 +254,10 @@ dvsg_status dvsg_set_timing(dvsg_ctx *ctx, int enabled);
  * assign, route, K1, combine, hit vectors), D2H start/end (copy stream).
  * out holds 6 x max_microbatches doubles; *n_out = microbatches written. */
 dvsg_status dvsg_last_pipeline_timeline(dvsg_ctx *ctx, double *out, int max_microbatches, int *n_out);
+/* Measured timeline of the last node-sharded bulk / NCCL search with timing
+ * on: per interval {kind (0 step kernel, 1 peer barrier or NCCL exchange),
+ * start ms, end ms} from the search start; out holds 3 x max_intervals. */
+dvsg_status dvsg_last_sharded_timeline(dvsg_ctx *ctx, double *out, int max_intervals, int *n_out);
 dvsg_status dvsg_last_timings(dvsg_ctx *ctx, float *search_ms, float *assign_ms,
                               float *combine_ms, float *total_ms);
 /* Number of library kernels launched by this context since creation. */

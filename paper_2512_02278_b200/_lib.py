@@ -86,6 +86,7 @@ _SIGS = {
     "dvsg_nccl_connect": (c_int, [c_void_p, c_void_p]),
     "dvsg_set_timing": (c_int, [c_void_p, c_int]),
     "dvsg_last_pipeline_timeline": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
+    "dvsg_last_sharded_timeline": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
     "dvsg_last_timings": (c_int, [c_void_p, P_f32, P_f32, P_f32, P_f32]),
     "dvsg_kernel_launches": (c_uint64, [c_void_p]),
     "dvsg_last_search_stats": (c_int, [c_void_p, P_u64, P_u64, P_u64]),

@@ -447,6 +447,18 @@ class Context:
         return out
 
 
+def _sharded_timeline(ctx, rank: int = 0) -> List[dict]:
+    buf = np.zeros(3 * 1024, np.float64)
+    n = ctypes.c_int(0)
+    check(lib.dvsg_last_sharded_timeline(ctx._h, _ptr(buf), 1024, ctypes.byref(n)))
+    return [{"rank": rank, "lane": "compute" if buf[3 * i] == 0 else "comm",
+             "stage": "xg_step" if buf[3 * i] == 0 else "exchange", "start": float(buf[3 * i + 1]),
+             "end": float(buf[3 * i + 2])} for i in range(n.value)]
+
+
+Context.last_sharded_timeline = _sharded_timeline
+
+
 TIMELINE_STAGE_ORDER = {"kmeans": 0, "dispatch": 1, "search": 2, "combine": 3}
 MEASURED_STAGE_ORDER = {"h2d": 0, "search": 1, "d2h": 2}
 

@@ -184,6 +184,9 @@ struct dvsg_ctx {
     bool issued = false;
   } xg;
 
+  // measured timeline of the last bulk-exchange search (timing on)
+  std::vector<int> xg_tl;                      // 0: step kernel, 1: barrier / NCCL exchange
+  std::vector<cudaEvent_t> xg_tl_ev;
   int shard_exchange = -1;                     // 0 bulk (default), 1 fused, 2 nccl; -1: env DVSG_SHARD_EXCHANGE
   // NCCL baseline of the bulk exchange (host-driven send/recv per phase)
   ncclComm_t nccl = nullptr;
@@ -604,6 +607,7 @@ void nccl_check(ncclResult_t r, const char* what) {
 // ---- node-sharded search, bulk-synchronous exchange (xchg_kernel.cu) -------
 constexpr size_t kXgHeader = 256;  // cursor [2][8] u32 @0, flags [8] u32 @64
 constexpr int kXgLanes = 4;
+constexpr size_t kXgTlMax = 1024;  // timeline intervals kept per search
 
 size_t xg_region_bytes(int nranks, uint64_t wcap, uint64_t maxraw, int dpad) {
   size_t b = kXgHeader;
@@ -807,10 +811,25 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
     la[l].hash = x.hash.p + so * k.hsize;
     la[l].meta = x.meta.p + so * (uint64_t)R;
   }
+  // measured timeline of this search (timing on): an event pair around every
+  // step kernel (compute lane) and every barrier / NCCL exchange (comm lane)
+  c->xg_tl.clear();
+  auto tl_mark = [&](int kind) -> int {
+    if (!c->timing || c->xg_tl.size() >= kXgTlMax) return -1;
+    const int i = (int)c->xg_tl.size();
+    c->xg_tl.push_back(kind);
+    cuda_check(cudaEventRecord(c->xg_tl_ev[2 * i], c->stream), "event");
+    return i;
+  };
+  auto tl_end = [&](int i) {
+    if (i >= 0) cuda_check(cudaEventRecord(c->xg_tl_ev[2 * i + 1], c->stream), "event");
+  };
   auto barrier = [&](int l) {
     if (emulate || use_nccl) return;  // stream order (+ NCCL) is the barrier
     x.epoch[l] += 1;
+    const int m = tl_mark(1);
     cuda_check(dvsg::launch_xg_barrier(la[l].views, R, me, x.epoch[l], x.err.p, c->stream), "xg barrier");
+    tl_end(m);
     c->launches += 1;
   };
   // Per lane the ops are E0 S0 E1 S1 ... E_I S_I E_{I+1} (E_{I+1}: finalize).
@@ -874,8 +893,10 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
       const dvsg::XgArgs& sa = la[std::max(0, ls >= 0 ? ls : le)];
       if (use_nccl && le >= 0)
         cuda_check(cudaMemsetAsync(n_cur, 0, (size_t)R * 2 * R * 4, c->stream), "cursor reset");
+      const int mk = tl_mark(0);
       cuda_check(dvsg::launch_xg_step(ea, sa, le >= 0, ls >= 0, x.counters.p + 2 * t, p->metric, p->accum,
                                       c->num_sms, c->stream), "xg step");
+      tl_end(mk);
       c->launches += 1;
       if (ls >= 0 && !use_nccl)  // that phase's inbox cursors are free again (next used two barriers later)
         for (int rr = 0; rr < rank_n; ++rr)
@@ -884,6 +905,7 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
       // requests (after an expand) / replies (after a score) delivered
       if (le >= 0 && la[le].phase <= p->iterations) barrier(le);
       if (ls >= 0) barrier(ls);
+      const int mx = use_nccl ? tl_mark(1) : -1;
       if (use_nccl && le >= 0 && la[le].phase <= p->iterations) {
         // requests: counts through the host (NCCL needs host-side sizes), then data
         const NcclApi& nc = nccl_api();
@@ -928,6 +950,7 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
         }
         nccl_check(nc.group_end(), "ncclGroupEnd");
       }
+      tl_end(mx);
     }
   }
   if (c->timing) {
@@ -1129,6 +1152,8 @@ dvsg_status dvsg_create(int device, dvsg_ctx** out) {
     for (auto& e : c->ev) cuda_check(cudaEventCreate(&e), "event");
     for (auto& e : c->mb_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (auto& e : c->tl_ev) cuda_check(cudaEventCreate(&e), "event");
+    c->xg_tl_ev.resize(2 * kXgTlMax);
+    for (auto& e : c->xg_tl_ev) cuda_check(cudaEventCreate(&e), "event");
     *out = c.release();
   });
 }
@@ -1145,6 +1170,7 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     for (auto& e : c->ev) cudaEventDestroy(e);
     for (auto& e : c->mb_ev) cudaEventDestroy(e);
     for (auto& e : c->tl_ev) cudaEventDestroy(e);
+    for (auto& e : c->xg_tl_ev) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->comm);
 
@@ -1803,6 +1829,25 @@ dvsg_status dvsg_last_pipeline_timeline(dvsg_ctx* c, double* out, int max_microb
         out[6 * i + e] = ms;
       }
     *n_out = m;
+  });
+}
+
+dvsg_status dvsg_last_sharded_timeline(dvsg_ctx* c, double* out, int max_intervals, int* n_out) {
+  return guarded([&] {
+    set_device(c);
+    *n_out = 0;
+    const int n = std::min((int)c->xg_tl.size(), max_intervals);
+    if (n == 0) return;
+    cuda_check(cudaEventSynchronize(c->xg_tl_ev[2 * (c->xg_tl.size() - 1) + 1]), "timeline");
+    for (int i = 0; i < n; ++i) {
+      float a = 0, b = 0;
+      cuda_check(cudaEventElapsedTime(&a, c->xg_tl_ev[0], c->xg_tl_ev[2 * i]), "elapsed");
+      cuda_check(cudaEventElapsedTime(&b, c->xg_tl_ev[0], c->xg_tl_ev[2 * i + 1]), "elapsed");
+      out[3 * i] = c->xg_tl[(size_t)i];
+      out[3 * i + 1] = a;
+      out[3 * i + 2] = b;
+    }
+    *n_out = n;
   });
 }
 
