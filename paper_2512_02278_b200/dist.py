@@ -162,3 +162,149 @@ def run_pipeline_distributed(ctx, d_q, p, fanout: int, placement, world: int, wi
             vectors = torch.where(hit_ok[:, :, None], vectors, torch.zeros_like(vectors))
         visited_total = int(u_vis.sum().item())
     return ids, dists, counts, vectors, visited_total
+
+
+def run_pipeline_distributed_mb(ctx, comm_ctx, d_q, p, fanout: int, placement, world: int,
+                                microbatches: int = 2, with_vectors: bool = True, group=None,
+                                timeline: bool = False, rank: int = 0):
+    """run_pipeline_distributed with the reference's microbatch schedule made
+    real (simulator.cpp:295-297 two_microbatch, replay_schedule :71-168):
+    per microbatch kmeans (assign + route) and search run on ctx's stream --
+    the compute lane -- while dispatch and combine (the all-to-alls, the
+    un-permute and the combine kernel, on comm_ctx's stream) run on the comm
+    lane, so microbatch i+1's dispatch overlaps microbatch i's search and
+    microbatch i's combine overlaps i+1's search.  comm_ctx is a second
+    context on the same device (its stream and kernels only; no index).
+    Returns (ids, dists, counts, vectors, visited_total, intervals): the
+    intervals are the reference's Timeline fields measured with CUDA events
+    (None unless timeline=True) and satisfy check_timeline."""
+    import torch
+    import torch.distributed as dist
+    dev = d_q.device
+    nq, dim = int(d_q.shape[0]), int(d_q.shape[1])
+    k, c = int(p.k), int(fanout)
+    m = max(1, min(int(microbatches), nq))
+    edges = [nq * i // m for i in range(m + 1)]
+    cs = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    xs = torch.cuda.ExternalStream(comm_ctx.stream, device=dev)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=timeline)
+
+    marks = {}
+    with torch.cuda.stream(xs):  # written on the comm lane (combine)
+        ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        counts = torch.empty((nq,), dtype=torch.int32, device=dev)
+        vectors = torch.zeros((nq, k, dim), dtype=torch.float32, device=dev) if with_vectors else None
+    with torch.cuda.stream(cs):  # written on the compute lane (kmeans)
+        assign = torch.empty((nq, c), dtype=torch.int32, device=dev)
+    plans = []
+    # kmeans stage of every microbatch on the compute lane
+    with torch.cuda.stream(cs):
+        for i in range(m):
+            q0, q1 = edges[i], edges[i + 1]
+            e0, e1 = ev(), ev()
+            e0.record(cs)
+            ctx.assign_top_c_device(d_q[q0:q1].data_ptr(), q1 - q0, dim, c, assign[q0:q1].data_ptr())
+            order, cnt = route_to_owners(assign[q0:q1], placement, world)
+            e1.record(cs)
+            marks[(i, "kmeans")] = (e0, e1)
+            plans.append((order, cnt))
+        send = torch.stack([pl[1] for pl in plans]).t().contiguous()  # world x m
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=group)  # sizes for every microbatch at once
+        sc = send.t().tolist()
+        rc = recv.t().tolist()
+    # dispatch of every microbatch on the comm lane (NCCL runs collectives in
+    # issue order, so all dispatches go ahead of the first combine)
+    recvd = []
+    for i in range(m):
+        q0, q1 = edges[i], edges[i + 1]
+        order = plans[i][0]
+        with torch.cuda.stream(xs):
+            xs.wait_event(marks[(i, "kmeans")][1])
+            d0, d1 = ev(), ev()
+            d0.record(xs)
+            nrecv = int(sum(rc[i]))
+            q_send = d_q[q0:q1].index_select(0, torch.div(order, c, rounding_mode="floor"))
+            cl_send = assign[q0:q1].reshape(-1).index_select(0, order)
+            q_recv = torch.empty((nrecv, dim), dtype=d_q.dtype, device=dev)
+            cl_recv = torch.empty((nrecv,), dtype=torch.int32, device=dev)
+            dist.all_to_all_single(q_recv, q_send, rc[i], sc[i], group=group)
+            dist.all_to_all_single(cl_recv, cl_send, rc[i], sc[i], group=group)
+            d1.record(xs)
+            marks[(i, "dispatch")] = (d0, d1)
+            recvd.append((q_recv, cl_recv, nrecv))
+    # every search is issued before the first combine: combine_results_device
+    # synchronizes the comm stream (unsorted-partial check), which must not
+    # hold back the next microbatch's search
+    results = []
+    for i in range(m):
+        q_recv, cl_recv, nrecv = recvd[i]
+        with torch.cuda.stream(cs):  # search on the compute lane
+            cs.wait_event(marks[(i, "dispatch")][1])
+            s0, s1 = ev(), ev()
+            s0.record(cs)
+            r_ids = torch.empty((nrecv, k), dtype=torch.int32, device=dev)
+            r_d = torch.empty((nrecv, k), dtype=torch.float32, device=dev)
+            r_cnt = torch.empty((nrecv,), dtype=torch.int32, device=dev)
+            r_vis = torch.empty((nrecv,), dtype=torch.int64, device=dev)
+            r_vec = torch.zeros((nrecv, k, dim), dtype=torch.float32, device=dev) if with_vectors else None
+            if nrecv:
+                uq = torch.arange(nrecv, dtype=torch.int32, device=dev)
+                ctx.search_units_device(q_recv.data_ptr(), nrecv, dim, uq.data_ptr(), cl_recv.data_ptr(), nrecv, p,
+                                        r_ids.data_ptr(), r_d.data_ptr(), r_cnt.data_ptr(), r_vis.data_ptr())
+                if with_vectors:
+                    ctx.gather_vectors_device(r_ids.data_ptr(), r_cnt.data_ptr(), nrecv, k, r_vec.data_ptr())
+            s1.record(cs)
+            marks[(i, "search")] = (s0, s1)
+            results.append((r_ids, r_d, r_cnt, r_vis, r_vec))
+    with torch.cuda.stream(xs):  # the comm lane owns every later read of it
+        visited_total = torch.zeros((), dtype=torch.int64, device=dev)
+    for i in range(m):
+        q0, q1 = edges[i], edges[i + 1]
+        n = q1 - q0
+        order = plans[i][0]
+        r_ids, r_d, r_cnt, r_vis, r_vec = results[i]
+        with torch.cuda.stream(xs):  # combine on the comm lane
+            xs.wait_event(marks[(i, "search")][1])
+            c0, c1 = ev(), ev()
+            c0.record(xs)
+            nu = n * c
+
+            def back(t, shape):
+                out = torch.empty(shape, dtype=t.dtype, device=dev)
+                dist.all_to_all_single(out, t, sc[i], rc[i], group=group)
+                u = torch.empty_like(out)
+                u[order] = out
+                return u
+
+            u_ids = back(r_ids, (nu, k))
+            u_d = back(r_d, (nu, k))
+            u_cnt = back(r_cnt, (nu,))
+            u_vis = back(r_vis, (nu,))
+            comm_ctx.combine_results_device(n, c, u_ids.data_ptr(), u_d.data_ptr(), u_cnt.data_ptr(), k, k,
+                                            ids[q0:q1].data_ptr(), dists[q0:q1].data_ptr(), counts[q0:q1].data_ptr())
+            if with_vectors:
+                u_vec = back(r_vec, (nu, k, dim)).view(n, c * k, dim)
+                part_ids = u_ids.view(n, c * k)
+                slot_ok = (torch.arange(k, device=dev)[None, None, :] < u_cnt.view(n, c, 1)).view(n, c * k)
+                hit_ok = torch.arange(k, device=dev)[None, :] < counts[q0:q1, None]
+                match = (part_ids[:, None, :] == ids[q0:q1, :, None]) & slot_ok[:, None, :]
+                src = match.int().argmax(dim=2)
+                got = torch.gather(u_vec, 1, src[:, :, None].expand(n, k, dim))
+                vectors[q0:q1] = torch.where(hit_ok[:, :, None], got, torch.zeros_like(got))
+            visited_total += u_vis.sum()  # stream-ordered on the comm lane
+            c1.record(xs)
+            marks[(i, "combine")] = (c0, c1)
+    torch.cuda.synchronize(dev)
+    visited_total = int(visited_total.item())
+    intervals = None
+    if timeline:
+        base = marks[(0, "kmeans")][0]
+        lane = {"kmeans": "compute", "search": "compute", "dispatch": "comm", "combine": "comm"}
+        intervals = [{"rank": rank, "lane": lane[s], "stage": s, "microbatch": i,
+                      "start": base.elapsed_time(a), "end": base.elapsed_time(b)}
+                     for (i, s), (a, b) in sorted(marks.items())]
+    return ids, dists, counts, vectors, visited_total, intervals

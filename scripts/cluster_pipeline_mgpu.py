@@ -90,6 +90,39 @@ def main():
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # the microbatched schedule (dispatch / combine overlapping search)
+    from paper_2512_02278_b200.dist import run_pipeline_distributed_mb
+    cctx = dvs.Context(local)
+    mb_out = {}
+    for mbs in (2, 4):
+        r = run_pipeline_distributed_mb(ctx, cctx, torch.from_numpy(qc).to(dev), p, a.fanout, placement, world,
+                                        microbatches=mbs)
+        ok_mb = bool(np.array_equal(r[2].cpu().numpy().view(np.uint32), want.counts) and r[4] == want.visited_total
+                     and np.array_equal(r[0].cpu().numpy().view(np.uint32), gi) and np.array_equal(r[3].cpu().numpy(), gv))
+        same_mb = torch.tensor([int(ok_mb)], device=dev)
+        dist.all_reduce(same_mb, op=dist.ReduceOp.MIN)
+        for _ in range(2):
+            run_pipeline_distributed_mb(ctx, cctx, d_q, p, a.fanout, placement, world, microbatches=mbs)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            run_pipeline_distributed_mb(ctx, cctx, d_q, p, a.fanout, placement, world, microbatches=mbs)
+        tt = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        r = run_pipeline_distributed_mb(ctx, cctx, d_q, p, a.fanout, placement, world, microbatches=mbs,
+                                        timeline=True, rank=rank)
+        tl = r[5]
+        msg = dvs.check_timeline(tl, stage_order={"kmeans": 0, "dispatch": 1, "search": 2, "combine": 3})
+        span = max(iv["end"] for iv in tl)
+        busy = {ln: sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == ln) for ln in ("compute", "comm")}
+        mb_out[str(mbs)] = {"qps": a.nq * world / (float(tt[0]) / a.steps / 1e3),
+                            "ms_per_step": float(tt[0]) / a.steps,
+                            "identical_to_one_gpu_pipeline_all_ranks": bool(same_mb[0]),
+                            "timeline_rank0": {"check_timeline": msg or "ok", "makespan_ms": span,
+                                               "compute_busy_ms": busy["compute"], "comm_busy_ms": busy["comm"]}}
+        if rank == 0 and mbs == 2:
+            with open(os.environ.get("TIMELINE_OUT", "/dev/null"), "w") as f:
+                json.dump(tl, f, indent=1)
     # recall on this rank's first 1000 queries
     truth = synth.brute_force_gt(data, queries[:1000], 10, ctx=full)
     rec = synth.recall_at_k(ids.cpu().numpy().view(np.uint32)[:1000], cnt[:1000], truth, 10)
@@ -101,6 +134,7 @@ def main():
             "qps": a.nq * world / (ms / 1e3), "ms_per_step": ms, "visited_per_query": vis / a.steps / a.nq,
             "recall_at_10_rank0": round(rec, 4), "identical_to_one_gpu_pipeline_all_ranks": bool(same[0]),
             "checked_queries_per_rank": a.check, "setup_s": round(setup_s, 1),
+            "microbatched": mb_out,
             "exchange": "NCCL all_to_all_single (torch.distributed): dispatch of (query, cluster) units, "
                         "results + hit vectors back"}), flush=True)
     dist.destroy_process_group()
