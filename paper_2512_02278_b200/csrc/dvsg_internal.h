@@ -137,7 +137,6 @@ struct XgArgs {
   uint32_t* out_count;
   uint64_t* out_visited;
   uint64_t out_stride;
-  unsigned long long* work_counter;
   unsigned long long* stats;  // [0] units, [1] visited, [2] expanded
   int* err;
 };
