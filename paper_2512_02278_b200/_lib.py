@@ -22,7 +22,7 @@ lib = ctypes.CDLL(LIB_PATH)
 
 DVSG_OK, DVSG_EINVAL, DVSG_EFORMAT, DVSG_EINTERNAL = 0, 2, 3, 4
 METRIC_L2, METRIC_IP = 0, 1
-ACCUM_F64, ACCUM_F32 = 0, 1
+ACCUM_F64, ACCUM_F32, ACCUM_F32C = 0, 1, 2
 
 
 class dvsg_search_params(ctypes.Structure):

@@ -33,7 +33,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import (ACCUM_F32, ACCUM_F64, METRIC_IP, METRIC_L2, FormatError, InternalError,
+from ._lib import (ACCUM_F32, ACCUM_F32C, ACCUM_F64, METRIC_IP, METRIC_L2, FormatError, InternalError,
                    InvalidArgument, check, lib)
 
 __all__ = [
@@ -69,11 +69,11 @@ class SearchParams:
     k: int = 10
     entry_count: int = 6
     metric: str = "l2"   # "l2" (squared_l2) | "ip" (-dot; parity unpinned)
-    accum: str = "f64"   # "f64" parity mode | "f32" fast mode
+    accum: str = "f64"   # "f64" parity mode | "f32" fast mode | "f32c" compensated f32
 
     def to_c(self) -> _lib.dvsg_search_params:
         metric = {"l2": METRIC_L2, "ip": METRIC_IP}.get(self.metric)
-        accum = {"f64": ACCUM_F64, "f32": ACCUM_F32}.get(self.accum)
+        accum = {"f64": ACCUM_F64, "f32": ACCUM_F32, "f32c": ACCUM_F32C}.get(self.accum)
         if metric is None:
             raise InvalidArgument(f"SearchParams: unknown metric {self.metric!r}")
         if accum is None:

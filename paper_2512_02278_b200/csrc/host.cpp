@@ -287,7 +287,8 @@ void validate_params(const dvsg_search_params* p) {
   if (p->iterations < 1 || p->beam_width < 1 || p->k < 1 || p->entry_count < 1)
     fail(DVSG_EINVAL, "SearchParams: iterations, beam_width, k and entry_count must all be >= 1");
   if (p->metric != DVSG_METRIC_L2 && p->metric != DVSG_METRIC_IP) fail(DVSG_EINVAL, "SearchParams: unknown metric %d", p->metric);
-  if (p->accum != DVSG_ACCUM_F64 && p->accum != DVSG_ACCUM_F32) fail(DVSG_EINVAL, "SearchParams: unknown accum %d", p->accum);
+  if (p->accum != DVSG_ACCUM_F64 && p->accum != DVSG_ACCUM_F32 && p->accum != DVSG_ACCUM_F32C)
+    fail(DVSG_EINVAL, "SearchParams: unknown accum %d", p->accum);
 }
 
 uint64_t pow2_at_least(uint64_t x) {
@@ -498,6 +499,7 @@ void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uin
   validate_params(p);
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
+  if (p->accum == DVSG_ACCUM_F32C) fail(DVSG_EINVAL, "sharded search: accum f32c is implemented by the single-GPU search only");
   if (nranks < 1 || nranks > 8) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
   if (c->dpad > 768) fail(DVSG_EINVAL, "sharded search: dim above 768 not supported");
   if (nq == 0) return;
@@ -654,6 +656,7 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
   validate_params(p);
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
+  if (p->accum == DVSG_ACCUM_F32C) fail(DVSG_EINVAL, "sharded search: accum f32c is implemented by the single-GPU search only");
   if (nranks < 1 || nranks > dvsg::kXgMaxRanks) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
   if (c->dpad > 768) fail(DVSG_EINVAL, "sharded search: dim above 768 not supported");
   if (nq == 0) return;

@@ -318,6 +318,36 @@ __device__ __forceinline__ uint64_t* sort_runs(uint64_t* s, int n, uint64_t* tmp
   return src;
 }
 
+// Compensated f32 accumulator (DVSG_ACCUM_F32C): hi carries the running
+// TwoSum of the rounded terms, lo the sum of every rounding error (TwoSum,
+// FMA TwoProd, and for L2 the exact-difference error).  ~48-bit effective
+// mantissa: agrees with the fp64 sum after the final f32 rounding except
+// within ~2^-24 ulp of a rounding boundary (an id-identity mode, not parity).
+struct F2 {
+  float hi, lo;
+};
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
+  const float s = __fadd_rn(a.hi, b.hi);
+  const float bb = __fsub_rn(s, a.hi);
+  const float e = __fadd_rn(__fsub_rn(a.hi, __fsub_rn(s, bb)), __fsub_rn(b.hi, bb));
+  return F2{s, __fadd_rn(e, __fadd_rn(a.lo, b.lo))};
+}
+__device__ __forceinline__ F2 operator+(F2 a, F2 b) { return f2_add(a, b); }
+__device__ __forceinline__ F2& operator+=(F2& a, F2 b) {
+  a = f2_add(a, b);
+  return a;
+}
+__device__ __forceinline__ float shfl_xor(float v, int off) { return __shfl_xor_sync(kFull, v, off); }
+__device__ __forceinline__ double shfl_xor(double v, int off) { return __shfl_xor_sync(kFull, v, off); }
+__device__ __forceinline__ F2 shfl_xor(F2 v, int off) {
+  return F2{__shfl_xor_sync(kFull, v.hi, off), __shfl_xor_sync(kFull, v.lo, off)};
+}
+// the accumulated sum rounded once to f32 (graph_index/distance.cpp: the
+// fp64 sum cast to float); negation commutes with round-to-nearest-even
+__device__ __forceinline__ float acc_to_f32(float v) { return v; }
+__device__ __forceinline__ float acc_to_f32(double v) { return (float)v; }
+__device__ __forceinline__ float acc_to_f32(F2 v) { return __fadd_rn(v.hi, v.lo); }
+
 // U partial sums per lane -> lane holds the full sum of vector
 // (lane >> (5 - log2 U)) & (U - 1): log2(U) "transpose" stages that halve the
 // live values, then a plain butterfly (U - 1 + 5 - log2 U shuffles instead of 5U).
@@ -333,12 +363,12 @@ __device__ __forceinline__ ACC transpose_reduce(ACC (&p)[U], int lane) {
     for (int i = 0; i < half; ++i) {
       const ACC send = upper ? p[i] : p[i + half];
       const ACC keep = upper ? p[i + half] : p[i];
-      p[i] = keep + __shfl_xor_sync(kFull, send, off);
+      p[i] = keep + shfl_xor(send, off);
     }
   }
   ACC v = p[0];
 #pragma unroll
-  for (int off = 16 >> LU; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  for (int off = 16 >> LU; off > 0; off >>= 1) v += shfl_xor(v, off);
   return v;
 }
 
@@ -362,6 +392,39 @@ __device__ __forceinline__ double lane_partial<double, 1>(const float4& x, const
   acc = __dadd_rn(acc, __dmul_rn((double)x.y, (double)q.y));
   acc = __dadd_rn(acc, __dmul_rn((double)x.z, (double)q.z));
   acc = __dadd_rn(acc, __dmul_rn((double)x.w, (double)q.w));
+  return acc;
+}
+// exact x - q as d + de (TwoSum), d^2 as p + pe (FMA TwoProd), the 2*d*de
+// cross term into lo (de^2 is below lo's own rounding)
+__device__ __forceinline__ void f2_sq_diff(float x, float q, F2& acc) {
+  const float d = __fsub_rn(x, q);
+  const float bb = __fsub_rn(d, x);
+  const float de = __fadd_rn(__fsub_rn(x, __fsub_rn(d, bb)), __fsub_rn(-q, bb));
+  const float p = __fmul_rn(d, d);
+  float lo = __fmaf_rn(d, d, -p);
+  lo = __fmaf_rn(__fmul_rn(2.0f, d), de, lo);
+  acc = f2_add(acc, F2{p, lo});
+}
+__device__ __forceinline__ void f2_prod(float x, float q, F2& acc) {
+  const float p = __fmul_rn(x, q);
+  acc = f2_add(acc, F2{p, __fmaf_rn(x, q, -p)});
+}
+template <>
+__device__ __forceinline__ F2 lane_partial<F2, 0>(const float4& x, const float4& q) {
+  F2 acc{0.f, 0.f};
+  f2_sq_diff(x.x, q.x, acc);
+  f2_sq_diff(x.y, q.y, acc);
+  f2_sq_diff(x.z, q.z, acc);
+  f2_sq_diff(x.w, q.w, acc);
+  return acc;
+}
+template <>
+__device__ __forceinline__ F2 lane_partial<F2, 1>(const float4& x, const float4& q) {
+  F2 acc{0.f, 0.f};
+  f2_prod(x.x, q.x, acc);
+  f2_prod(x.y, q.y, acc);
+  f2_prod(x.z, q.z, acc);
+  f2_prod(x.w, q.w, acc);
   return acc;
 }
 template <>

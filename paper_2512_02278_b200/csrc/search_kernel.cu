@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           bool pass = false;
           uint64_t mykey = 0;
           if ((lane & ((32 >> LU) - 1)) == 0 && ci < M) {
-            const float dist = METRIC == 0 ? (float)tot : (float)(-tot);
+            const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
             mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
             pass = mykey < thresh;
           }
@@ -437,6 +437,12 @@ cudaError_t launch_v(const SearchArgs& a, int metric, int accum, int num_sms, in
                                  : launch_t<VPL, double, 0, false>(a, num_sms, mg, s, g);
     return full ? launch_t<VPL, double, 1, true>(a, num_sms, mg, s, g)
                 : launch_t<VPL, double, 1, false>(a, num_sms, mg, s, g);
+  }
+  if (accum == 2) {
+    if (metric == 0) return full ? launch_t<VPL, F2, 0, true>(a, num_sms, mg, s, g)
+                                 : launch_t<VPL, F2, 0, false>(a, num_sms, mg, s, g);
+    return full ? launch_t<VPL, F2, 1, true>(a, num_sms, mg, s, g)
+                : launch_t<VPL, F2, 1, false>(a, num_sms, mg, s, g);
   }
   if (metric == 0) return full ? launch_t<VPL, float, 0, true>(a, num_sms, mg, s, g)
                                : launch_t<VPL, float, 0, false>(a, num_sms, mg, s, g);

@@ -102,7 +102,7 @@ __device__ __forceinline__ void score_ids(const uint32_t* cand, int M, const flo
     const bool valid = (lane & ((32 >> LU) - 1)) == 0 && ci < M;
     uint64_t key = 0;
     if (valid) {
-      const float dist = METRIC == 0 ? (float)tot : (float)(-tot);
+      const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
       key = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
     }
     sink(valid, ci, key);

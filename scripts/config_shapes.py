@@ -111,10 +111,23 @@ def main():
         r64 = ctx.beam_search(0, queries[:m], p64)
         agree = float(np.mean([np.array_equal(got[i, :counts[i]], r64[0][i, :r64[2][i]]) for i in range(m)]))
         st = vis.cpu().numpy().mean()
+        # compensated f32 (accum "f32c"): speed and id agreement with f64
+        p = dvs.SearchParams(6, sh["beam"], sh["k"], sh["beam"], metric=sh["metric"], accum="f32c")
+        ms32c = timed()
+        got_c = ids.cpu().numpy().view(np.uint32)
+        counts_c = cnt.cpu().numpy().view(np.uint32)
+        agree_c = float(np.mean([np.array_equal(got_c[i, :counts_c[i]], r64[0][i, :r64[2][i]]) for i in range(m)]))
+        d64 = r64[1]
+        dc = dists.cpu().numpy()
+        rel = max(float(np.max(np.abs(dc[i, :counts_c[i]] - d64[i, :r64[2][i]]) /
+                               np.maximum(np.abs(d64[i, :r64[2][i]]), 1e-30)))
+                  for i in range(m) if counts_c[i] > 0 and np.array_equal(got_c[i, :counts_c[i]], r64[0][i, :r64[2][i]]))
         line = {"shape": sh["name"], "n": sh["n"], "dim": sh["dim"], "metric": sh["metric"], "k": k,
                 "beam": sh["beam"], "iterations": 6, "queries": nq, "qps": nq / (ms / 1e3), "ms_per_batch": ms,
                 "recall_at_k": round(rec, 4), "visited_per_query": float(st),
                 "f32_ids_identical_to_f64_mode": agree, "qps_f64_parity_mode": nq / (ms64 / 1e3),
+                "qps_f32c_mode": nq / (ms32c / 1e3), "f32c_ids_identical_to_f64_mode": agree_c,
+                "f32c_max_rel_dist_diff_vs_f64": rel,
                 "setup_s": round(build_s, 1)}
         print(json.dumps(line), flush=True)
         if out:

@@ -570,3 +570,35 @@ def test_brute_force_topk_matches_reference(ctx, golden, oracle):
     assert np.array_equal(gi, wi) and np.array_equal(gd, wd)
     with pytest.raises(dvs.InvalidArgument):
         ctx.brute_force_topk(v[:5], q, 6)
+
+
+@pytest.mark.parametrize("metric,dim", [("l2", 768), ("ip", 768), ("l2", 96)])
+def test_compensated_f32_matches_reference_on_float_data(ctx, oracle, metric, dim):
+    # accum "f32c": TwoSum / FMA-TwoProd pairs instead of fp64.  Not a parity
+    # mode: ids must agree with the reference on >= 99.9% of queries and
+    # distances within 1e-6 relative (tighter than the north_star 1e-4).
+    n = 2000
+    v = oracle.random_dataset(n, dim, 91)
+    if metric == "ip":
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+    adj = oracle.build_graph(v, 24)
+    eo = oracle.compute_entry_order(v)
+    q = oracle.random_dataset(256, dim, 92)
+    gids = np.arange(n, dtype=np.uint32)
+    want = oracle.beam_search(v, gids, adj, eo, q, 4, 32, 10, 32, metric=1 if metric == "ip" else 0)
+    gi, gd, gc, gv = _search(ctx, v, adj, q, dvs.SearchParams(4, 32, 10, 32, metric=metric, accum="f32c"), gids)
+    wi, wd, wc, wv = want
+    same = sum(int(gc[i]) == int(wc[i]) and np.array_equal(gi[i, :wc[i]], wi[i, :wc[i]]) for i in range(len(q)))
+    assert same >= 0.999 * len(q), (same, len(q))
+    for i in range(len(q)):
+        np.testing.assert_allclose(gd[i, :wc[i]], wd[i, :wc[i]], rtol=1e-6, atol=1e-7)
+
+
+def test_compensated_f32_rejected_by_sharded_search(ctx, oracle):
+    v = sift_like(500, 16, 4, 93)
+    adj = oracle.build_graph(v, 8)
+    ctx.reset()
+    ctx._single_key = None
+    ctx.load_partition(0, _graph(v, adj))
+    with pytest.raises(dvs.InvalidArgument):
+        ctx.beam_search_sharded_emulated(2, v[:4], dvs.SearchParams(2, 8, 5, 8, accum="f32c"))
