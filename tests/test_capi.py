@@ -89,3 +89,14 @@ def test_save_index_rejects_unbuilt():
     import paper_2512_02278_b200 as dvs
     with pytest.raises(dvs.InvalidArgument):
         dvs.save_index(dvs.BuiltIndex(np.zeros((0, 4), np.float32), np.zeros(0, np.uint32), 1, 4), "/tmp/x")
+
+
+def test_search_params_accum_modes():
+    # f64 parity / f32 fast / f32c compensated; anything else is invalid_argument
+    import paper_2512_02278_b200 as dvs
+    from paper_2512_02278_b200 import _lib
+    assert (_lib.ACCUM_F64, _lib.ACCUM_F32, _lib.ACCUM_F32C) == (0, 1, 2)
+    for name, code in (("f64", 0), ("f32", 1), ("f32c", 2)):
+        assert dvs.SearchParams(6, 64, 10, 64, accum=name).to_c().accum == code
+    with pytest.raises(dvs.InvalidArgument):
+        dvs.SearchParams(6, 64, 10, 64, accum="f16").to_c()
