@@ -47,7 +47,7 @@ typedef int dvsg_status;
 
 #define DVSG_ACCUM_F64 0 /* fp64 lane partials + fp64 tree, rounded once to f32 (parity mode) */
 #define DVSG_ACCUM_F32 1 /* fp32 lane partials + fp32 tree (fast mode) */
-#define DVSG_ACCUM_F32C 2 /* compensated fp32 (TwoSum / FMA TwoProd pairs): ~48-bit sums, single-GPU search only */
+#define DVSG_ACCUM_F32C 2 /* compensated fp32 (TwoSum / FMA TwoProd pairs): ~48-bit sums */
 
 typedef struct dvsg_ctx dvsg_ctx;
 

@@ -499,7 +499,6 @@ void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uin
   validate_params(p);
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
-  if (p->accum == DVSG_ACCUM_F32C) fail(DVSG_EINVAL, "sharded search: accum f32c is implemented by the single-GPU search only");
   if (nranks < 1 || nranks > 8) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
   if (c->dpad > 768) fail(DVSG_EINVAL, "sharded search: dim above 768 not supported");
   if (nq == 0) return;
@@ -656,7 +655,6 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
   validate_params(p);
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
-  if (p->accum == DVSG_ACCUM_F32C) fail(DVSG_EINVAL, "sharded search: accum f32c is implemented by the single-GPU search only");
   if (nranks < 1 || nranks > dvsg::kXgMaxRanks) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
   if (c->dpad > 768) fail(DVSG_EINVAL, "sharded search: dim above 768 not supported");
   if (nq == 0) return;

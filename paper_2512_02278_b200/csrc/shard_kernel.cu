@@ -551,6 +551,10 @@ cudaError_t launch_sh_v(const SearchArgs& a, const ShardArgs& sh, int metric, in
     return metric == 0 ? launch_sh_t<VPL, double, 0>(a, sh, num_sms, s, g, gpr, per_sm)
                        : launch_sh_t<VPL, double, 1>(a, sh, num_sms, s, g, gpr, per_sm);
   }
+  if (accum == 2) {
+    return metric == 0 ? launch_sh_t<VPL, F2, 0>(a, sh, num_sms, s, g, gpr, per_sm)
+                       : launch_sh_t<VPL, F2, 1>(a, sh, num_sms, s, g, gpr, per_sm);
+  }
   return metric == 0 ? launch_sh_t<VPL, float, 0>(a, sh, num_sms, s, g, gpr, per_sm)
                      : launch_sh_t<VPL, float, 1>(a, sh, num_sms, s, g, gpr, per_sm);
 }

@@ -428,7 +428,7 @@ __device__ __forceinline__ void expand_unit(const XgArgs& a, const int rr, const
           bool pass = false;
           uint64_t key = 0;
           if ((lane & ((32 >> LU) - 1)) == 0 && ci < cnt) {
-            const float dist = METRIC == 0 ? (float)tot : (float)(-tot);
+            const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
             key = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)ids[ci] << 1);
             pass = key < thresh;
           }
@@ -567,7 +567,7 @@ __device__ __forceinline__ void score_warp_block(const XgArgs& a, const ScoreTab
             load_query<VPL, FULL>(q, qbase + (uint64_t)qid * (uint32_t)a.dpad, lane, a.dim);
           }
           const float* row = lbase + (uint64_t)((uint32_t)rq[u] - lo) * (uint32_t)a.dpad;
-          ACC acc = 0;
+          ACC acc{};
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             const float4 xv = (FULL || lane * 4 + 128 * v < a.dpad) ? ldg_f4(row + 128 * v) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -579,7 +579,7 @@ __device__ __forceinline__ void score_warp_block(const XgArgs& a, const ScoreTab
       const ACC tot = transpose_reduce<U, ACC>(part, lane);
       if ((lane & ((32 >> LU) - 1)) == 0) {
         const int e = round * U + ((lane >> (5 - LU)) & (U - 1));
-        const float dist = METRIC == 0 ? (float)tot : (float)(-tot);
+        const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
         wk[e] = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)(uint32_t)wq[e] << 1);
       }
     }
@@ -690,6 +690,12 @@ cudaError_t launch_step_v(const XgArgs& ea, const XgArgs& sa, int do_e, int do_s
                                  : launch_step_t<VPL, double, 0, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
     return full ? launch_step_t<VPL, double, 1, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
                 : launch_step_t<VPL, double, 1, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
+  }
+  if (accum == 2) {
+    if (metric == 0) return full ? launch_step_t<VPL, F2, 0, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
+                                 : launch_step_t<VPL, F2, 0, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
+    return full ? launch_step_t<VPL, F2, 1, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
+                : launch_step_t<VPL, F2, 1, false>(ea, sa, do_e, do_s, ctr, num_sms, s);
   }
   if (metric == 0) return full ? launch_step_t<VPL, float, 0, true>(ea, sa, do_e, do_s, ctr, num_sms, s)
                                : launch_step_t<VPL, float, 0, false>(ea, sa, do_e, do_s, ctr, num_sms, s);

@@ -594,11 +594,22 @@ def test_compensated_f32_matches_reference_on_float_data(ctx, oracle, metric, di
         np.testing.assert_allclose(gd[i, :wc[i]], wd[i, :wc[i]], rtol=1e-6, atol=1e-7)
 
 
-def test_compensated_f32_rejected_by_sharded_search(ctx, oracle):
-    v = sift_like(500, 16, 4, 93)
-    adj = oracle.build_graph(v, 8)
-    ctx.reset()
-    ctx._single_key = None
-    ctx.load_partition(0, _graph(v, adj))
-    with pytest.raises(dvs.InvalidArgument):
-        ctx.beam_search_sharded_emulated(2, v[:4], dvs.SearchParams(2, 8, 5, 8, accum="f32c"))
+@pytest.mark.parametrize("exchange", ["bulk", "fused"])
+@pytest.mark.parametrize("metric,dim", [("l2", 768), ("ip", 96)])
+def test_compensated_f32_sharded_equals_unsharded(ctx, oracle, exchange, metric, dim):
+    # same pair arithmetic in K1 and in both sharded kernels: bit-identical
+    n = 1500
+    v = oracle.random_dataset(n, dim, 95)
+    if metric == "ip":
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+    adj = oracle.build_graph(v, 16)
+    eo = oracle.compute_entry_order(v)
+    q = oracle.random_dataset(64, dim, 96)
+    p = dvs.SearchParams(4, 16, 10, 16, metric=metric, accum="f32c")
+    want = _search(ctx, v, adj, q, p, None, eo)
+    ctx.set_shard_exchange(exchange)
+    try:
+        got = ctx.beam_search_sharded_emulated(3, q, p)
+    finally:
+        ctx.set_shard_exchange("bulk")
+    _assert_same(got, want, True, f"f32c sharded {exchange} {metric}")
