@@ -403,7 +403,11 @@ __device__ __forceinline__ void f2_sq_diff(float x, float q, F2& acc) {
   const float p = __fmul_rn(d, d);
   float lo = __fmaf_rn(d, d, -p);
   lo = __fmaf_rn(__fmul_rn(2.0f, d), de, lo);
-  acc = f2_add(acc, F2{p, lo});
+  // both addends >= 0: FastTwoSum on (max, min) is error-free
+  const float a = fmaxf(acc.hi, p), b = fminf(acc.hi, p);
+  const float s = __fadd_rn(a, b);
+  const float e = __fsub_rn(b, __fsub_rn(s, a));
+  acc = F2{s, __fadd_rn(acc.lo, __fadd_rn(e, lo))};
 }
 __device__ __forceinline__ void f2_prod(float x, float q, F2& acc) {
   const float p = __fmul_rn(x, q);

@@ -18,18 +18,24 @@ def main():
     ap.add_argument("--accum", default="f32c")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--nq", type=int, default=20_000)
+    ap.add_argument("--metric", default="ip")
+    ap.add_argument("--dim", type=int, default=768)
+    ap.add_argument("--time", action="store_true")
     a = ap.parse_args()
     import paper_2512_02278_b200 as dvs
     ctx = dvs.Context(0)
-    data = normalised(200_000, 768, 32, 1)
-    queries = normalised(a.nq, 768, 32, 2)
+    data = normalised(200_000, a.dim, 32, 1)
+    queries = normalised(a.nq, a.dim, 32, 2)
     adj = ctx.build_graph(data, 32)
     ctx.load_partition(0, dvs.GraphIndex(data, np.arange(len(data), dtype=np.uint32), 32, adj,
                                          dvs.compute_entry_order(data)))
-    p = dvs.SearchParams(6, 256, 100, 256, metric="ip", accum=a.accum)
-    for _ in range(a.reps):
+    p = dvs.SearchParams(6, 256, 100, 256, metric=a.metric, accum=a.accum)
+    import time
+    for r in range(a.reps):
+        t0 = time.perf_counter()
         ids, dists, counts, visited = ctx.beam_search(0, queries, p)
-    print("ok", a.accum, float(visited.mean()))
+        dt = time.perf_counter() - t0
+    print("ok", a.accum, a.metric, a.dim, float(visited.mean()), "qps(host-timed, last rep)=%.0f" % (a.nq / dt) if a.time else "")
 
 
 if __name__ == "__main__":
