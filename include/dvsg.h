@@ -46,7 +46,8 @@ typedef int dvsg_status;
 #define DVSG_METRIC_IP 1 /* -dot (distance.cpp:35-42); extension, parity unpinned */
 
 #define DVSG_ACCUM_F64 0 /* fp64 lane partials + fp64 tree, rounded once to f32 (parity mode) */
-#define DVSG_ACCUM_F32 1 /* fp32 lane partials + fp32 tree (fast mode) */
+#define DVSG_ACCUM_F32 1 /* fp32 lane partials + fp32 tree (fast mode); exact on integer-valued
+                          data, upgraded to F32C / F64 on anything else (dvsg_index_integral) */
 #define DVSG_ACCUM_F32C 2 /* compensated fp32 (TwoSum / FMA TwoProd pairs): ~48-bit sums */
 
 typedef struct dvsg_ctx dvsg_ctx;
@@ -242,6 +243,87 @@ dvsg_status dvsg_build_graph(dvsg_ctx *ctx, const float *vectors, uint64_t n, in
 dvsg_status dvsg_brute_force_topk(dvsg_ctx *ctx, const float *db, uint64_t n, int dim,
                                   const float *queries, uint64_t nq, int k, uint32_t *out_ids,
                                   float *out_dists);
+
+/* ---- large-index construction on the device (csrc/ivf_build.cu) ----------
+ * The pieces a 10M-100M-row index is built from without leaving HBM.  All
+ * pointers are device pointers on the context's device; every call is
+ * synchronous (it returns after its kernels finished).
+ *
+ * K7 range top-m: for each block, the rows [row0, row0+nrows) (nrows <= 128)
+ * of d_rows against the column ranges ranges[list_off[list] ..
+ * list_off[list+1]) (pairs {begin, end} of d_cols rows, disjoint): the m <= 32
+ * smallest (squared L2, column id) keys -- the ordering of scored_less
+ * (dataset.hpp:33-46) -- written to rows out_row0 + i of d_out_ids /
+ * d_out_dists (nullable), out_stride entries per row.  Distances use the dot
+ * form over precomputed fp32 norms (dvsg_row_norms_device): exact on
+ * integer-valued data below 2^24 per term.  Serves the cluster-restricted
+ * graph build that stands in for build_graph (graph_index.cpp:46-97) at
+ * 10^16-pair sizes, nearest-centroid assignment, and brute-force ground truth
+ * (topk.cpp:12-30) split over column ranges.  Missing entries (fewer than m
+ * candidates) are id 0xFFFFFFFF / +inf, or with DVSG_RANGE_BUILD_PAD the
+ * valid ones repeated cyclically (graph_index.cpp:86-92).  d_row_map
+ * (nullable): block row i reads physical row d_row_map[row0 + i] of d_rows
+ * (and its norm), so a permuted view needs no gathered copy. */
+typedef struct {
+  uint32_t row0, nrows, list, out_row0;
+} dvsg_range_block;
+#define DVSG_RANGE_EXCLUDE_SELF 1 /* skip column == row (d_rows == d_cols) */
+#define DVSG_RANGE_BUILD_PAD 2
+#define DVSG_RANGE_MERGE 4 /* start from the lists already in d_out_ids / d_out_dists (ids
+                              0xFFFFFFFF = empty): several passes over disjoint ranges give
+                              the top-m of their union */
+#define DVSG_RANGE_OUT_PHYSICAL 8 /* outputs (and merge inputs) at row d_row_map[row0 + i] */
+dvsg_status dvsg_range_topk_device(dvsg_ctx *ctx, const float *d_rows, const float *d_row_norms,
+                                   const float *d_cols, const float *d_col_norms, int dpad,
+                                   const uint32_t *d_row_map, const dvsg_range_block *d_blocks,
+                                   uint64_t nblocks,
+                                   const uint32_t *d_list_off, const uint32_t *d_ranges, int m,
+                                   int flags, uint32_t *d_out_ids, float *d_out_dists,
+                                   uint64_t out_stride);
+/* fp32 squared norms of n rows of dpad floats */
+dvsg_status dvsg_row_norms_device(dvsg_ctx *ctx, const float *d_x, uint64_t n, int dpad,
+                                  float *d_out);
+/* Segment means for the clustering: d_cents[s] = f32(fp64 in-order sum of
+ * rows d_idx[d_off[s] .. d_off[s+1]) / count) (d_idx NULL: rows d_off[s]..);
+ * empty segments keep their centroid.  Deterministic (no atomics). */
+dvsg_status dvsg_segment_means_device(dvsg_ctx *ctx, const float *d_x, int dpad,
+                                      const uint32_t *d_idx, const uint64_t *d_off, uint32_t nseg,
+                                      float *d_cents);
+/* compute_entry_order (graph_index.cpp:21-44) on the device, bit-exact: fp64
+ * column sums in row order, f32 mean, fp64 sequential squared_l2 per row,
+ * sort by (f32 dist, id).  dim <= 1024. */
+dvsg_status dvsg_compute_entry_order_device(dvsg_ctx *ctx, const float *d_x, uint64_t n, int dim,
+                                            int dpad, uint32_t *d_out);
+/* Build a partition in place: reserves n rows in the context's index arrays
+ * and returns device pointers to them (vectors n x dpad with dpad = dim
+ * rounded up to 4, pad columns zeroed; adjacency n x out_degree local ids;
+ * global ids; entry order), which the caller fills; then commit validates it
+ * on the device (ids in range, finite, pad zero) and makes it resident, like
+ * dvsg_load_partition without a host copy of a 50 GB index. */
+dvsg_status dvsg_partition_alloc_device(dvsg_ctx *ctx, uint32_t cluster, uint64_t n, int dim,
+                                        int out_degree, float **d_vectors, uint32_t **d_adjacency,
+                                        uint32_t **d_global_ids, uint32_t **d_entry_order);
+#define DVSG_COMMIT_ENTRY_ORDER 1 /* compute the entry order on the device */
+#define DVSG_COMMIT_IOTA_IDS 2    /* global ids = 0..n-1 */
+dvsg_status dvsg_partition_commit_device(dvsg_ctx *ctx, int flags);
+/* CAGRA-style optimisation of a kNN graph (rows sorted by distance), in
+ * place on device adjacency (n x out_degree local ids, n < 2^27, degree
+ * <= 32): rank-based detour pruning keeps `keep` forward edges per row, the
+ * rest of each row becomes reverse edges (in-edges closest in forward rank
+ * first), then the remaining forward edges; no duplicates.  Deterministic.
+ * The search (graph_index.cpp:105-187) is unchanged; only its graph is. */
+dvsg_status dvsg_optimize_graph_device(dvsg_ctx *ctx, uint32_t *d_adjacency, uint64_t n,
+                                       int out_degree, int keep);
+/* Read-only device pointers to a resident partition's arrays (vectors
+ * n x dpad, adjacency n x out_degree, global ids, entry order), valid until
+ * the next index change. */
+dvsg_status dvsg_partition_view_device(dvsg_ctx *ctx, uint32_t cluster, const float **d_vectors,
+                                       const uint32_t **d_adjacency, const uint32_t **d_global_ids,
+                                       const uint32_t **d_entry_order, uint64_t *n);
+/* 1 when every resident row is integer-valued below 2^24, i.e. the fp32 fast
+ * mode is exact; otherwise DVSG_ACCUM_F32 searches run in DVSG_ACCUM_F32C
+ * (inner product or dim >= 384) or DVSG_ACCUM_F64. */
+dvsg_status dvsg_index_integral(dvsg_ctx *ctx, int *out);
 
 /* ---- instrumentation ---------------------------------------------------- */
 /* Device time (ms) of the last search kernel launch (K1) and of the whole

@@ -361,9 +361,11 @@ class Ref:
         sizes = [g[0].shape[0] for g in graphs]
         offs = np.zeros(len(graphs) + 1, np.uint64)
         offs[1:] = np.cumsum(sizes)
-        vec = np.ascontiguousarray(np.concatenate([g[0] for g in graphs]), np.float32)
-        adj = np.ascontiguousarray(np.concatenate([np.asarray(g[1]).reshape(-1) for g in graphs]), np.uint32)
-        gids = np.ascontiguousarray(np.concatenate([g[2] for g in graphs]), np.uint32)
+        def cat(parts, dt):  # no concatenated copy of a single (possibly 50 GB) graph
+            return np.ascontiguousarray(parts[0] if len(parts) == 1 else np.concatenate(parts), dt)
+        vec = cat([g[0] for g in graphs], np.float32)
+        adj = cat([np.asarray(g[1]).reshape(-1) for g in graphs], np.uint32)
+        gids = cat([g[2] for g in graphs], np.uint32)
         h = self.lib.dvsref_index_from_arrays(cents.shape[0], cents.shape[1], out_degree, _p(cents),
                                               _p(ctr), ranks, _p(offs), _p(vec), _p(adj), _p(gids))
         if not h:

@@ -23,6 +23,8 @@ lib = ctypes.CDLL(LIB_PATH)
 DVSG_OK, DVSG_EINVAL, DVSG_EFORMAT, DVSG_EINTERNAL = 0, 2, 3, 4
 METRIC_L2, METRIC_IP = 0, 1
 ACCUM_F64, ACCUM_F32, ACCUM_F32C = 0, 1, 2
+RANGE_EXCLUDE_SELF, RANGE_BUILD_PAD, RANGE_MERGE, RANGE_OUT_PHYSICAL = 1, 2, 4, 8
+COMMIT_ENTRY_ORDER, COMMIT_IOTA_IDS = 1, 2
 
 
 class dvsg_search_params(ctypes.Structure):
@@ -91,6 +93,19 @@ _SIGS = {
     "dvsg_kernel_launches": (c_uint64, [c_void_p]),
     "dvsg_last_search_stats": (c_int, [c_void_p, P_u64, P_u64, P_u64]),
     "dvsg_debug_counters": (c_int, [c_void_p, c_void_p]),
+    "dvsg_row_norms_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p]),
+    "dvsg_range_topk_device": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
+                                       c_void_p, c_uint64, c_void_p, c_void_p, c_int, c_int, c_void_p,
+                                       c_void_p, c_uint64]),
+    "dvsg_segment_means_device": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_uint32, c_void_p]),
+    "dvsg_compute_entry_order_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
+    "dvsg_partition_alloc_device": (c_int, [c_void_p, c_uint32, c_uint64, c_int, c_int, POINTER(c_void_p),
+                                            POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p)]),
+    "dvsg_partition_commit_device": (c_int, [c_void_p, c_int]),
+    "dvsg_index_integral": (c_int, [c_void_p, POINTER(c_int)]),
+    "dvsg_optimize_graph_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int]),
+    "dvsg_partition_view_device": (c_int, [c_void_p, c_uint32, POINTER(c_void_p), POINTER(c_void_p),
+                                           POINTER(c_void_p), POINTER(c_void_p), POINTER(c_uint64)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -420,6 +420,53 @@ class Context:
         return ids, dists
 
     # ---- timing --------------------------------------------------------------
+    # ---- large-index construction (device pointers, synchronous) -----------
+    def row_norms_device(self, d_x: int, n: int, dpad: int, d_out: int) -> None:
+        check(lib.dvsg_row_norms_device(self._h, d_x, n, dpad, d_out))
+
+    def range_topk_device(self, d_rows: int, d_row_norms: int, d_cols: int, d_col_norms: int, dpad: int,
+                          d_row_map: int, d_blocks: int, nblocks: int, d_list_off: int, d_ranges: int,
+                          m: int, flags: int, d_out_ids: int, d_out_dists: int, out_stride: int) -> None:
+        check(lib.dvsg_range_topk_device(self._h, d_rows, d_row_norms, d_cols, d_col_norms, dpad,
+                                         d_row_map or None, d_blocks or None, nblocks, d_list_off or None,
+                                         d_ranges or None, m, flags, d_out_ids, d_out_dists or None,
+                                         out_stride))
+
+    def segment_means_device(self, d_x: int, dpad: int, d_idx: int, d_off: int, nseg: int,
+                             d_cents: int) -> None:
+        check(lib.dvsg_segment_means_device(self._h, d_x, dpad, d_idx or None, d_off, nseg, d_cents))
+
+    def compute_entry_order_device(self, d_x: int, n: int, dim: int, dpad: int, d_out: int) -> None:
+        check(lib.dvsg_compute_entry_order_device(self._h, d_x, n, dim, dpad, d_out))
+
+    def partition_alloc_device(self, cluster: int, n: int, dim: int, out_degree: int):
+        """-> (d_vectors, d_adjacency, d_global_ids, d_entry_order) pointers into the
+        context's index arrays (dvsg_partition_alloc_device)."""
+        v, a, g, e = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib.dvsg_partition_alloc_device(self._h, int(cluster), int(n), int(dim), int(out_degree),
+                                              ctypes.byref(v), ctypes.byref(a), ctypes.byref(g),
+                                              ctypes.byref(e)))
+        return int(v.value or 0), int(a.value or 0), int(g.value or 0), int(e.value or 0)
+
+    def partition_commit_device(self, flags: int) -> None:
+        check(lib.dvsg_partition_commit_device(self._h, int(flags)))
+
+    def partition_view_device(self, cluster: int):
+        """-> (d_vectors, d_adjacency, d_global_ids, d_entry_order, n) of a resident partition."""
+        v, a, g, e, n = (ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(),
+                         ctypes.c_uint64())
+        check(lib.dvsg_partition_view_device(self._h, int(cluster), ctypes.byref(v), ctypes.byref(a),
+                                             ctypes.byref(g), ctypes.byref(e), ctypes.byref(n)))
+        return int(v.value or 0), int(a.value or 0), int(g.value or 0), int(e.value or 0), int(n.value)
+
+    def optimize_graph_device(self, d_adjacency: int, n: int, out_degree: int, keep: int) -> None:
+        check(lib.dvsg_optimize_graph_device(self._h, d_adjacency, int(n), int(out_degree), int(keep)))
+
+    def index_integral(self) -> bool:
+        out = ctypes.c_int()
+        check(lib.dvsg_index_integral(self._h, ctypes.byref(out)))
+        return bool(out.value)
+
     def set_timing(self, on: bool) -> None:
         check(lib.dvsg_set_timing(self._h, 1 if on else 0))
 

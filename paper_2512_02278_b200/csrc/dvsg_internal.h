@@ -193,6 +193,44 @@ cudaError_t launch_reduce_u64(const uint64_t* in, uint64_t n, unsigned long long
 cudaError_t launch_brute_force(const float* queries, uint64_t nq, const float* db, uint64_t n,
                                int dpad, int k, uint32_t* out_ids, float* out_dists,
                                cudaStream_t stream);
+// ---- large-index construction (ivf_build.cu) -------------------------------
+// One K7 work item: rows [row0, row0 + nrows) (nrows <= 128) against the
+// column ranges ranges[list_off[list] .. list_off[list + 1]); outputs go to
+// rows out_row0 + i of out_ids / out_dists (out_stride entries per row).
+struct RangeBlock {
+  uint32_t row0, nrows, list, out_row0;
+};
+// flags: bit 0 exclude column == row (rows and cols are the same array);
+// bit 1 build_graph padding (cyclic repeat of short lists); bit 2 merge into the
+// lists already in out_ids / out_dists (multi-pass); bit 3 output row = the
+// physical row (row_map[row0 + r]) instead of out_row0 + r.  row_map (nullable):
+// block row r reads physical row row_map[row0 + r] of `rows` (norms likewise).
+cudaError_t launch_range_topk(const float* rows, const float* rnorm, const float* cols,
+                              const float* cnorm, int dpad, const uint32_t* row_map, const RangeBlock* blocks,
+                              uint64_t nblocks, const uint32_t* list_off, const uint2* ranges,
+                              int m, int flags, uint32_t* out_ids, float* out_dists,
+                              uint64_t out_stride, cudaStream_t stream);
+size_t range_topk_smem_bytes();
+cudaError_t launch_row_norms(const float* x, uint64_t n, int dpad, float* out, cudaStream_t stream);
+// Exact compute_entry_order on the device (dim <= 1024).
+size_t entry_order_scratch_bytes(uint64_t n);
+cudaError_t launch_entry_order(const float* x, uint64_t n, int dim, int dpad, void* scratch,
+                               size_t scratch_bytes, uint32_t* out, cudaStream_t stream);
+// Partition validators: *flag |= 1 (adjacency id >= n), 4 (non-finite),
+// 16 (not integer-valued below 2^24), 32 (non-zero pad column), 64 (gids not
+// strictly increasing; gids may be null).
+cudaError_t launch_check_partition(const float* x, uint64_t n, int dim, int dpad, const uint32_t* adj,
+                                   int dg, const uint32_t* gids, int* flag, cudaStream_t stream);
+cudaError_t launch_iota(uint32_t* out, uint64_t n, cudaStream_t stream);
+cudaError_t launch_segment_means(const float* x, int dpad, const uint32_t* idx, const uint64_t* off,
+                                 uint32_t nseg, float* cents, cudaStream_t stream);
+
+// CAGRA-style rank-based pruning + reverse edges of a kNN graph, in place
+// (graph_opt.cu); n < 2^27, 2 <= d <= 32.
+size_t graph_opt_scratch_bytes(uint64_t n, int d, int keep);
+cudaError_t launch_graph_optimize(uint32_t* adj, uint64_t n, int d, int keep, void* scratch,
+                                  size_t scratch_bytes, cudaStream_t stream);
+
 // K6 exact kNN graph rows (knn_build.cu)
 cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad,
                              int out_degree, uint32_t* adjacency, cudaStream_t stream);

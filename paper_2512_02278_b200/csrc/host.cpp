@@ -114,6 +114,15 @@ bool finite_all(const float* x, uint64_t n) {
   return true;
 }
 
+// integer-valued with |x| < 2^24: every fp32 squared-L2 / dot sum the fast
+// mode forms is then exact (at the dims the bench uses), i.e. equal to the
+// reference's fp64-then-round arithmetic (distance.cpp:19-27)
+bool integral_all(const float* x, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i)
+    if (!(x[i] == std::nearbyint(x[i]) && std::fabs(x[i]) < 16777216.f)) return false;
+  return true;
+}
+
 }  // namespace
 
 struct dvsg_ctx {
@@ -129,6 +138,12 @@ struct dvsg_ctx {
   DevBuf<uint32_t> adj, gids, entry;
   std::vector<dvsg::PartDesc> parts;
   std::vector<char> part_mono;     // global ids strictly increasing in local id (per part)
+  bool all_integral = true;        // every resident row integer-valued below 2^24 (fp32 sums exact)
+  struct Pending {                 // dvsg_partition_alloc_device .. commit
+    bool active = false;
+    uint32_t cluster = 0;
+    uint64_t n = 0, r0 = 0;
+  } pend;
   DevBuf<dvsg::PartDesc> d_parts;
   bool parts_dirty = true;
   // routing table
@@ -291,6 +306,19 @@ void validate_params(const dvsg_search_params* p) {
     fail(DVSG_EINVAL, "SearchParams: unknown accum %d", p->accum);
 }
 
+// The fp32 fast mode (DVSG_ACCUM_F32) is exact only when every sum it forms
+// is exact, i.e. on integer-valued data (checked at upload, all_integral).  On
+// anything else it is upgraded to a mode that meets the parity bar:
+// compensated f32 for inner product / wide rows (faster than f64 there), f64
+// otherwise.  DVSG_ALLOW_F32_FLOAT=1 keeps plain f32 (measurements only).
+dvsg_search_params effective_params(const dvsg_ctx* c, const dvsg_search_params* p) {
+  dvsg_search_params e = *p;
+  static const bool allow = env_u64("DVSG_ALLOW_F32_FLOAT", 0) != 0;
+  if (e.accum == DVSG_ACCUM_F32 && !c->all_integral && !allow)
+    e.accum = (e.metric == DVSG_METRIC_IP || c->dim >= 384) ? DVSG_ACCUM_F32C : DVSG_ACCUM_F64;
+  return e;
+}
+
 uint64_t pow2_at_least(uint64_t x) {
   uint64_t p = 1;
   while (p < x) p <<= 1;
@@ -383,6 +411,8 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
                   const uint32_t* d_up, uint64_t nunits, const dvsg_search_params* p,
                   uint32_t* d_ids, float* d_dists, uint32_t* d_count, uint64_t* d_visited) {
   validate_params(p);
+  const dvsg_search_params pe = effective_params(c, p);
+  p = &pe;
   if (c->sh.active) fail(DVSG_EINVAL, "beam_search: this context holds one rank's shard; use dvsg_search_sharded_device");
   if (c->parts.empty()) fail(DVSG_EINVAL, "beam_search: empty graph");
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
@@ -497,6 +527,8 @@ void search_sharded(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uin
                     const dvsg_search_params* p, uint32_t* d_ids, float* d_dists, uint32_t* d_count,
                     uint64_t* d_visited) {
   validate_params(p);
+  const dvsg_search_params pe = effective_params(c, p);
+  p = &pe;
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
   if (nranks < 1 || nranks > 8) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
@@ -653,6 +685,8 @@ void search_xchg(dvsg_ctx* c, bool emulate, int nranks, const float* d_q, uint64
                  const dvsg_search_params* p, uint32_t* d_ids, float* d_dists, uint32_t* d_count,
                  uint64_t* d_visited) {
   validate_params(p);
+  const dvsg_search_params pe = effective_params(c, p);
+  p = &pe;
   if (dim != c->dim) fail(DVSG_EINVAL, "beam_search: query dim %d != index dim %d", dim, c->dim);
   if (c->parts.size() != 1) fail(DVSG_EINVAL, "sharded search: the context must hold exactly one (whole-graph) partition");
   if (nranks < 1 || nranks > dvsg::kXgMaxRanks) fail(DVSG_EINVAL, "sharded search: nranks %d outside 1..8", nranks);
@@ -1195,6 +1229,8 @@ dvsg_status dvsg_index_reset(dvsg_ctx* c) {
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
     c->parts.clear();
     c->part_mono.clear();
+    c->all_integral = true;
+    c->pend = dvsg_ctx::Pending{};
     c->rows = 0;
     c->dim = c->dpad = c->dg = 0;
     c->clusters = 0;
@@ -1286,6 +1322,7 @@ dvsg_status dvsg_load_partition(dvsg_ctx* c, uint32_t cluster, uint64_t n, int d
     cuda_check(cudaMemcpy(c->entry.p + r0, entry_order, n * 4, cudaMemcpyHostToDevice), "entry H2D");
     c->parts.push_back(dvsg::PartDesc{r0, (uint32_t)n, cluster});
     c->part_mono.push_back(ids_increasing(global_ids, n));
+    c->all_integral = c->all_integral && integral_all(vectors, n * (uint64_t)dim);
     c->rows = r1;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = c->anchors_dirty = true;
   });
@@ -1443,6 +1480,7 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
     cuda_check(cudaMemcpy(c->entry.p, entry_order, n_total * 4, cudaMemcpyHostToDevice), "entry H2D");
     c->parts.push_back(dvsg::PartDesc{0, (uint32_t)n_total, 0});
     c->part_mono.push_back(global_ids ? ids_increasing(global_ids, n_total) : 1);
+    c->all_integral = integral_all(shard_vectors, (hi - lo) * (uint64_t)dim);
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
     auto& sh = c->sh;
     if (sh.arena) cudaFree(sh.arena);
@@ -1786,6 +1824,176 @@ dvsg_status dvsg_brute_force_topk(dvsg_ctx* c, const float* db, uint64_t n, int 
   });
 }
 
+// ---- large-index construction on the device (ivf_build.cu) ---------------
+
+dvsg_status dvsg_row_norms_device(dvsg_ctx* c, const float* d_x, uint64_t n, int dpad, float* d_out) {
+  return guarded([&] {
+    set_device(c);
+    if (dpad < 4 || dpad % 4) fail(DVSG_EINVAL, "row_norms: dpad %d must be a positive multiple of 4", dpad);
+    cuda_check(dvsg::launch_row_norms(d_x, n, dpad, d_out, c->stream), "row norms");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "row norms");
+  });
+}
+
+dvsg_status dvsg_range_topk_device(dvsg_ctx* c, const float* d_rows, const float* d_row_norms,
+                                   const float* d_cols, const float* d_col_norms, int dpad,
+                                   const uint32_t* d_row_map, const dvsg_range_block* d_blocks, uint64_t nblocks,
+                                   const uint32_t* d_list_off, const uint32_t* d_ranges, int m,
+                                   int flags, uint32_t* d_out_ids, float* d_out_dists,
+                                   uint64_t out_stride) {
+  static_assert(sizeof(dvsg_range_block) == sizeof(dvsg::RangeBlock), "range block layout");
+  return guarded([&] {
+    set_device(c);
+    if (m < 1 || m > 32) fail(DVSG_EINVAL, "range_topk: m=%d outside 1..32", m);
+    if (dpad < 4 || dpad % 4) fail(DVSG_EINVAL, "range_topk: dpad %d must be a positive multiple of 4", dpad);
+    if ((uint64_t)m > out_stride) fail(DVSG_EINVAL, "range_topk: out_stride %llu < m", (unsigned long long)out_stride);
+    if ((flags & DVSG_RANGE_MERGE) && !d_out_dists) fail(DVSG_EINVAL, "range_topk: DVSG_RANGE_MERGE needs d_out_dists");
+    if (!d_rows || !d_cols || !d_row_norms || !d_col_norms || !d_out_ids || (nblocks && (!d_blocks || !d_list_off || !d_ranges)))
+      fail(DVSG_EINVAL, "range_topk: null input");
+    cuda_check(dvsg::launch_range_topk(d_rows, d_row_norms, d_cols, d_col_norms, dpad, d_row_map,
+                                       reinterpret_cast<const dvsg::RangeBlock*>(d_blocks), nblocks,
+                                       d_list_off, reinterpret_cast<const uint2*>(d_ranges), m, flags,
+                                       d_out_ids, d_out_dists, out_stride, c->stream), "range_topk");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "range_topk");
+  });
+}
+
+dvsg_status dvsg_segment_means_device(dvsg_ctx* c, const float* d_x, int dpad, const uint32_t* d_idx,
+                                      const uint64_t* d_off, uint32_t nseg, float* d_cents) {
+  return guarded([&] {
+    set_device(c);
+    if (dpad < 1) fail(DVSG_EINVAL, "segment_means: dpad %d", dpad);
+    cuda_check(dvsg::launch_segment_means(d_x, dpad, d_idx, d_off, nseg, d_cents, c->stream), "segment means");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "segment means");
+  });
+}
+
+namespace {
+void entry_order_device(dvsg_ctx* c, const float* d_x, uint64_t n, int dim, int dpad, uint32_t* d_out) {
+  if (n == 0 || dim < 1) fail(DVSG_EINVAL, "compute_entry_order: empty partition");
+  if (dim > 1024) fail(DVSG_EINVAL, "compute_entry_order (device): dim %d above 1024", dim);
+  const size_t bytes = dvsg::entry_order_scratch_bytes(n);
+  DevBuf<unsigned char> scratch;
+  scratch.reserve(bytes, c->stream);
+  cuda_check(dvsg::launch_entry_order(d_x, n, dim, dpad, scratch.p, bytes, d_out, c->stream), "entry order");
+  c->launches += 4;
+  cuda_check(cudaStreamSynchronize(c->stream), "entry order");
+}
+}  // namespace
+
+dvsg_status dvsg_compute_entry_order_device(dvsg_ctx* c, const float* d_x, uint64_t n, int dim, int dpad,
+                                            uint32_t* d_out) {
+  return guarded([&] {
+    set_device(c);
+    if (dpad < dim || dpad % 4) fail(DVSG_EINVAL, "compute_entry_order: dpad %d (dim %d)", dpad, dim);
+    entry_order_device(c, d_x, n, dim, dpad, d_out);
+  });
+}
+
+dvsg_status dvsg_partition_alloc_device(dvsg_ctx* c, uint32_t cluster, uint64_t n, int dim, int out_degree,
+                                        float** d_vectors, uint32_t** d_adjacency, uint32_t** d_global_ids,
+                                        uint32_t** d_entry_order) {
+  return guarded([&] {
+    set_device(c);
+    if (c->pend.active) fail(DVSG_EINVAL, "partition_alloc: partition %u not committed yet", c->pend.cluster);
+    if (c->sh.active) fail(DVSG_EINVAL, "partition_alloc: this context holds one rank's shard");
+    if (n == 0) fail(DVSG_EINVAL, "BuiltIndex: empty partition");
+    if (n >= (1ull << 31)) fail(DVSG_EINVAL, "load_partition: %llu rows exceed the 2^31 local-id limit", (unsigned long long)n);
+    if (dim < 1) fail(DVSG_EINVAL, "Dataset: dim must be positive, got %d", dim);
+    if (out_degree < 1) fail(DVSG_EINVAL, "build_graph: out_degree must be >= 1");
+    if (c->dim && c->dim != dim) fail(DVSG_EINVAL, "BuiltIndex: graph dim mismatch (%d vs %d)", dim, c->dim);
+    if (c->dg && c->dg != out_degree) fail(DVSG_EINVAL, "BuiltIndex: graph out-degree mismatch (%d vs %d)", out_degree, c->dg);
+    if (slot_of(c, cluster) >= 0) fail(DVSG_EINVAL, "load_partition: cluster %u already resident", cluster);
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    const int dpad = (dim + 3) & ~3;
+    const uint64_t r0 = c->rows, r1 = r0 + n;
+    c->vec.reserve(r1 * (uint64_t)dpad, c->stream, true, r0 * (uint64_t)dpad);
+    c->adj.reserve(r1 * (uint64_t)out_degree, c->stream, true, r0 * (uint64_t)out_degree);
+    c->gids.reserve(r1, c->stream, true, r0);
+    c->entry.reserve(r1, c->stream, true, r0);
+    c->dim = dim;
+    c->dpad = dpad;
+    c->dg = out_degree;
+    if (dpad != dim) cuda_check(cudaMemset(c->vec.p + r0 * dpad, 0, n * (uint64_t)dpad * 4), "pad");
+    c->pend = dvsg_ctx::Pending{true, cluster, n, r0};
+    if (d_vectors) *d_vectors = c->vec.p + r0 * dpad;
+    if (d_adjacency) *d_adjacency = c->adj.p + r0 * out_degree;
+    if (d_global_ids) *d_global_ids = c->gids.p + r0;
+    if (d_entry_order) *d_entry_order = c->entry.p + r0;
+  });
+}
+
+dvsg_status dvsg_partition_commit_device(dvsg_ctx* c, int flags) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->pend.active) fail(DVSG_EINVAL, "partition_commit: no partition allocated");
+    const auto pd = c->pend;
+    c->pend.active = false;  // a failed commit drops the partition
+    const float* v = c->vec.p + pd.r0 * c->dpad;
+    uint32_t* gids = c->gids.p + pd.r0;
+    if (flags & DVSG_COMMIT_IOTA_IDS) cuda_check(dvsg::launch_iota(gids, pd.n, c->stream), "iota");
+    c->err_flag.reserve(1, c->stream);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "flag");
+    cuda_check(dvsg::launch_check_partition(v, pd.n, c->dim, c->dpad, c->adj.p + pd.r0 * c->dg, c->dg, gids,
+                                            c->err_flag.p, c->stream), "check partition");
+    int flag = 0;
+    cuda_check(cudaMemcpyAsync(&flag, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "flag");
+    cuda_check(cudaStreamSynchronize(c->stream), "check partition");
+    c->launches += 2;
+    if (flag & 1) fail(DVSG_EFORMAT, "index file: neighbor id out of range in cluster %u", pd.cluster);
+    if (flag & 4) fail(DVSG_EINVAL, "Dataset: non-finite element in partition %u", pd.cluster);
+    if (flag & 32) fail(DVSG_EINVAL, "partition_commit: pad columns %d..%d must be zero", c->dim, c->dpad - 1);
+    if (flags & DVSG_COMMIT_ENTRY_ORDER) entry_order_device(c, v, pd.n, c->dim, c->dpad, c->entry.p + pd.r0);
+    c->parts.push_back(dvsg::PartDesc{pd.r0, (uint32_t)pd.n, pd.cluster});
+    c->part_mono.push_back((flag & 64) == 0);
+    c->all_integral = c->all_integral && (flag & 16) == 0;
+    c->rows = pd.r0 + pd.n;
+    c->parts_dirty = c->slot_dirty = c->locator_dirty = c->anchors_dirty = true;
+  });
+}
+
+dvsg_status dvsg_optimize_graph_device(dvsg_ctx* c, uint32_t* d_adjacency, uint64_t n, int out_degree,
+                                       int keep) {
+  return guarded([&] {
+    set_device(c);
+    if (out_degree < 2 || out_degree > 32) fail(DVSG_EINVAL, "optimize_graph: out_degree %d outside 2..32", out_degree);
+    if (keep < 1 || keep > out_degree) fail(DVSG_EINVAL, "optimize_graph: keep %d outside 1..%d", keep, out_degree);
+    if (n == 0 || n >= (1ull << 27)) fail(DVSG_EINVAL, "optimize_graph: n %llu outside 1..2^27", (unsigned long long)n);
+    const size_t bytes = dvsg::graph_opt_scratch_bytes(n, out_degree, keep);
+    DevBuf<unsigned char> scratch;
+    scratch.reserve(bytes, c->stream);
+    cuda_check(dvsg::launch_graph_optimize(d_adjacency, n, out_degree, keep, scratch.p, bytes, c->stream), "optimize graph");
+    c->launches += 5;
+    cuda_check(cudaStreamSynchronize(c->stream), "optimize graph");
+  });
+}
+
+dvsg_status dvsg_partition_view_device(dvsg_ctx* c, uint32_t cluster, const float** d_vectors,
+                                       const uint32_t** d_adjacency, const uint32_t** d_global_ids,
+                                       const uint32_t** d_entry_order, uint64_t* n) {
+  return guarded([&] {
+    const int32_t s = slot_of(c, cluster);
+    if (s < 0) fail(DVSG_EINVAL, "cluster %u not resident", cluster);
+    const auto& pd = c->parts[(size_t)s];
+    if (c->sh.active) fail(DVSG_EINVAL, "partition_view: this context holds one rank's shard");
+    if (d_vectors) *d_vectors = c->vec.p + pd.row_off * c->dpad;
+    if (d_adjacency) *d_adjacency = c->adj.p + pd.row_off * c->dg;
+    if (d_global_ids) *d_global_ids = c->gids.p + pd.row_off;
+    if (d_entry_order) *d_entry_order = c->entry.p + pd.row_off;
+    if (n) *n = pd.n;
+  });
+}
+
+dvsg_status dvsg_index_integral(dvsg_ctx* c, int* out) {
+  return guarded([&] {
+    if (!out) fail(DVSG_EINVAL, "index_integral: null out");
+    *out = c->all_integral ? 1 : 0;
+  });
+}
+
 dvsg_status dvsg_set_shard_exchange(dvsg_ctx* c, int mode) {
   return guarded([&] {
     if (mode < 0 || mode > 2) fail(DVSG_EINVAL, "set_shard_exchange: mode %d (0 bulk, 1 fused, 2 nccl)", mode);
@@ -1986,6 +2194,8 @@ dvsg_status dvsg_load_index_file(dvsg_ctx* c, const char* path, int rank) {
     // all structural checks passed: reset and upload the owned partitions
     c->parts.clear();
     c->part_mono.clear();
+    c->all_integral = true;
+    c->pend = dvsg_ctx::Pending{};
     c->rows = 0;
     c->dim = c->dpad = c->dg = 0;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
