@@ -2,37 +2,53 @@
 """bench.py -- QPS of the batched graph search at recall@10 >= 0.95 on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dvsg|reference]
+                    [--workload cfg3|cfg1]
 
-One step = one run_pipeline pass (simulator.cpp:245-337 functional part:
+Workloads (BASELINE.json configs):
+  cfg3 (default) -- configs[2], the north-star config: Deep-like synthetic
+        100M x 96 (integer-valued f32, rank-16 latent), degree-32 graph built
+        on the GPU (cluster-restricted kNN + CAGRA-style rank pruning and
+        reverse edges, paper_2512_02278_b200/ivf.py), 1M-query batch per GPU
+        per step, top-10, beam 64, I=10, entry 64 (calibrated: recall@10
+        >= 0.95 against brute-force ground truth on a 2,000-query sample).
+  cfg1 -- configs[1] at N=1: 1M x 128, exact kNN-32 graph, 100k queries, I=6.
+
+One step = one run_pipeline pass (simulator.cpp:245-337, functional part:
 assign -> route -> K1 beam search -> combine -> attach hit vectors) over one
-batch of 100k synthetic SIFT-like queries against the 1M x 128 kNN-32 graph
-(BASELINE.json configs[1] at N=1: the graph in one partition; I=6, w=64,
-entry=64, k=10 calibrated to recall@10 >= 0.95 on this data).
+batch of queries.  At N > 1 (torchrun, one rank per GPU; `--gpus N` alone
+self-launches torchrun) the headline is the north-star layout: the index's
+vectors node-sharded across the N GPUs with the NVLink frontier exchange
+(xchg_kernel.cu), each rank the origin of its own 1M-query batch (weak
+scaling); full-replica searches are measured beside it.
 
-`value`  : device-resident queries, CUDA events on the library's stream, L2
-           flushed (256 MiB write) before every step, max over ranks.
-`e2e`    : the same step through the public host-buffer call
-           (dvsg_run_pipeline: pinned host queries in, ids/dists/counts/hit
-           vectors out; H2D and D2H inside the timed region).
-`roofline`: K1 algorithmic bytes (visited*4d + expanded*4*d_g + 4d per unit,
-           SURVEY 8d) / K1 event time, against MEASURED_PEAKS.json hbm_gbs.
+`value`     : device-resident queries, CUDA events on the library's stream,
+              max over ranks.  The 38 GB index is far larger than L2 and a
+              256 MiB buffer is written before every step.
+`e2e`       : the same step through the public host-buffer call
+              (dvsg_run_pipeline): pinned host queries in, ids / dists /
+              counts / hit vectors out, H2D and D2H inside the timed region;
+              `e2e.pageable` repeats it with ordinary (pageable) numpy buffers.
+`roofline`  : K1 algorithmic bytes (visited*4d + expanded*4*d_g + 4d per unit,
+              SURVEY 8d) / K1 event time, against MEASURED_PEAKS.json hbm_gbs;
+              `traffic` = ncu dram__bytes of K1 on the same config
+              (profiles/k1_traffic.json; ncu cannot run inside the timed run).
 `cpu_baseline`: the reference's own run_pipeline (oracle/_ref, compiled from
-           /root/reference sources) on a bounded query sample, all host cores.
-
-N > 1 (torchrun, one rank per GPU): each rank holds a full replica of the
-index and searches its own 100k-query batch ("replicas": weak scaling); the
-sharded frontier-exchange mode is not in this round.
-`--impl reference`: rank 0 times the reference CPU path (same config and
-metric), other ranks exit 0.
+              /root/reference sources) on a bounded query sample, all host cores.
+`--impl reference`: rank 0 times the reference's run_pipeline on the same
+              graph (built on the GPU by a separate setup process that writes
+              it to /dev/shm, so the timing process maps no libdvsg code).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
+import tempfile
 import time
 
 import numpy as np
@@ -41,41 +57,69 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+METRIC = "QPS at recall@10>=0.95"
+
+WORKLOADS = {
+    "cfg3": dict(n=100_000_000, dim=96, nq=1_000_000, iterations=10, beam=64, entry=64, k=10, degree=32,
+                 graph="ivf",
+                 desc="BASELINE configs[2]: Deep-like synthetic 100M x 96 (integer-valued f32, rank-16 "
+                      "latent), degree-32 graph (GPU-built: cluster-restricted kNN + CAGRA-style rank "
+                      "pruning / reverse edges) in 1 partition, 1M-query batch per GPU, top-10, beam 64, "
+                      "I=10, entry 64"),
+    "cfg1": dict(n=1_000_000, dim=128, nq=100_000, iterations=6, beam=64, entry=64, k=10, degree=32,
+                 graph="exact",
+                 desc="BASELINE configs[1] at N=1: SIFT-like synthetic 1M x 128 (integer-valued f32, "
+                      "rank-16 latent), exact kNN-32 graph in 1 partition, 100k-query batch per GPU, "
+                      "top-10, beam 64, I=6, entry 64"),
+}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", choices=["dvsg", "reference"], default="dvsg")
-    ap.add_argument("--n", "--rows", dest="n", type=int, default=1_000_000)
-    ap.add_argument("--nq", type=int, default=100_000)
-    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--impl", choices=["dvsg", "reference", "reference-setup"], default="dvsg")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3")
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=None)
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--dim", type=int, default=None)
     ap.add_argument("--rank-latent", type=int, default=16)
-    ap.add_argument("--degree", type=int, default=32)
-    ap.add_argument("--iterations", type=int, default=6)
-    ap.add_argument("--beam", type=int, default=64)
-    ap.add_argument("--k", type=int, default=10)
-    ap.add_argument("--entry", type=int, default=64)
-    ap.add_argument("--accum", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--degree", type=int, default=None)
+    ap.add_argument("--iterations", type=int, default=None)
+    ap.add_argument("--beam", type=int, default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--entry", type=int, default=None)
+    ap.add_argument("--accum", choices=["f32", "f64", "f32c"], default="f32")
+    ap.add_argument("--probe", type=int, default=8, help="cfg3 graph build: clusters probed per row")
+    ap.add_argument("--cluster-size", type=int, default=1024, help="cfg3 graph build: rows per cluster")
     ap.add_argument("--recall-sample", type=int, default=2000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=5.0,
+                    help="--impl reference: CPU seconds per timed step (sample size)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-modes", action="store_true", help="skip the f64 / f32c side measurement")
     ap.add_argument("--cache", default="/tmp/dvsg_bench_cache")
+    ap.add_argument("--ref-out", default=None, help=argparse.SUPPRESS)
     ap.add_argument("--mode", choices=["auto", "replica", "sharded"], default="auto",
-                    help="N>1 layout: full index per GPU, or node-sharded vectors with an NVLink "
-                         "frontier exchange (auto = replica headline, sharded measured beside it)")
+                    help="N>1 layout: auto = node-sharded headline with replicas measured beside it")
     ap.add_argument("--timeline-out", default=None,
                     help="write the measured e2e pipeline timeline (intervals JSON) here")
     ap.add_argument("--no-nccl-baseline", action="store_true",
                     help="skip the NCCL-exchange baseline measured beside the sharded mode at N>1")
     ap.add_argument("--exchange", choices=["bulk", "fused", "nccl"], default="bulk",
-                    help="sharded-mode exchange: bulk-synchronous phases (xchg_kernel.cu) or "
-                         "per-CTA round trips (shard_kernel.cu), or the bulk protocol over "
-                         "host-driven NCCL send/recv (the measured baseline)")
-    return ap.parse_args()
+                    help="sharded-mode exchange: bulk-synchronous phases (xchg_kernel.cu), per-CTA "
+                         "round trips (shard_kernel.cu), or the bulk protocol over host-driven NCCL "
+                         "send/recv (the measured baseline)")
+    a = ap.parse_args(argv)
+    for key, v in WORKLOADS[a.workload].items():
+        if key in ("graph", "desc"):
+            continue
+        if getattr(a, key) is None:
+            setattr(a, key, v)
+    a.graph = WORKLOADS[a.workload]["graph"]
+    return a
 
 
 def log(*a):
@@ -142,9 +186,83 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def sha256_bytes(a: np.ndarray) -> str:
+    h = hashlib.sha256()
+    mv = memoryview(np.ascontiguousarray(a)).cast("B")
+    step = 1 << 28
+    for b in range(0, len(mv), step):
+        h.update(mv[b:b + step])
+    return h.hexdigest()
+
+
+def recall_at_k(ids, counts, truth, k):
+    """recall_at_k, topk.cpp:32-49, averaged over queries."""
+    tot = 0.0
+    for q in range(truth.shape[0]):
+        tot += len(set(ids[q, :int(counts[q])].tolist()) & set(truth[q, :k].tolist())) / k
+    return tot / truth.shape[0]
+
+
 # ---------------------------------------------------------------------------
-def workload(args, rank: int, ctx):
-    """Data + queries + index (graph cached by config under args.cache)."""
+class Workload:
+    """The index resident in `ctx`, this rank's queries on the device, and
+    the ground truth of the recall sample."""
+
+    def __init__(self):
+        self.info = {}
+        self.graph_sha256 = None
+
+
+def build_cfg3(args, rank, ctx, dev, gt_rows=None):
+    """Data, graph and queries of the cfg3 workload, all built on the GPU
+    (setup, never timed)."""
+    import torch
+    from paper_2512_02278_b200 import ivf
+    t0 = time.time()
+    dpad = (args.dim + 3) // 4 * 4
+    x = ivf.sift_like_device(args.n, args.dim, args.rank_latent, seed=1, device=dev, dpad=dpad)
+    info = ivf.build_graph_ivf(ctx, x, degree=args.degree, cluster_size=args.cluster_size, probe=args.probe,
+                               dim=args.dim, optimize=True, log=log)
+    del x
+    info.pop("perm")
+    torch.cuda.empty_cache()
+    pv, pa, _, _, n = ctx.partition_view_device(0)
+    vec = ivf.device_view(pv, (n, dpad), torch.float32, dev)
+    # the routing table of a 1-partition index (C = 1): fp64 mean -> f32
+    acc = torch.zeros(dpad, dtype=torch.float64, device=dev)
+    for b in range(0, n, 1 << 24):
+        acc += vec[b:b + (1 << 24)].double().sum(0)
+    cent = (acc / n).float()[:args.dim].cpu().numpy()[None, :]
+    ctx.set_centroids(cent, np.zeros(1, np.uint32), 1)
+    q = ivf.sift_like_queries_device(args.nq, args.dim, args.rank_latent, data_seed=1, seed=2 + rank,
+                                     device=dev)
+    s = min(args.recall_sample, args.nq) if gt_rows is None else gt_rows
+    gt, _ = ivf.brute_force_topk(ctx, vec, ivf.row_norms(ctx, vec), q[:s].contiguous(), args.k)
+    w = Workload()
+    w.queries = q
+    w.gt = gt.cpu().numpy()
+    w.centroid = cent
+    w.vec = vec
+    w.adj = ivf.device_view(pa, (n, args.degree), torch.int32, dev)
+    w.info = {k: v for k, v in info.items()}
+    w.info["setup_s"] = time.time() - t0
+    log(f"[bench] cfg3 workload ready in {w.info['setup_s']:.1f}s")
+    return w
+
+
+def build_cfg1(args, rank, ctx, dev, gt_rows=None):
+    """The round-1 workload: numpy SIFT-like data, exact K6 graph (cached)."""
+    import torch
     from paper_2512_02278_b200 import synth
     from paper_2512_02278_b200.api import BuiltIndex, GraphIndex, compute_entry_order
     t0 = time.time()
@@ -159,102 +277,186 @@ def workload(args, rank: int, ctx):
     else:
         adj = ctx.build_graph(data, args.degree)       # K6, exact on integer data
         eo = compute_entry_order(data)                 # graph_index.cpp:21-44
-        tmp = adj_path + f".{os.getpid()}.npy"
-        np.save(tmp, adj)
-        os.replace(tmp, adj_path)
-        tmp = eo_path + f".{os.getpid()}.npy"
-        np.save(tmp, eo)
-        os.replace(tmp, eo_path)
+        for path, arr in ((adj_path, adj), (eo_path, eo)):
+            tmp = path + f".{os.getpid()}.npy"
+            np.save(tmp, arr)
+            os.replace(tmp, path)
     gids = np.arange(args.n, dtype=np.uint32)
     cents = data.mean(0, dtype=np.float64).astype(np.float32)[None, :]
-    index = BuiltIndex(cents, np.zeros(1, np.uint32), 1, args.degree,
-                       [GraphIndex(data, gids, args.degree, adj, eo)])
-    log(f"[bench] workload ready in {time.time() - t0:.1f}s")
-    return data, queries, index
+    index = BuiltIndex(cents, np.zeros(1, np.uint32), 1, args.degree, [GraphIndex(data, gids, args.degree, adj, eo)])
+    ctx.load_index(index)
+    s = min(args.recall_sample, args.nq) if gt_rows is None else gt_rows
+    w = Workload()
+    w.queries = torch.from_numpy(queries).to(dev)
+    w.gt = synth.brute_force_gt(data, queries[:s], args.k, ctx=ctx)
+    w.centroid = cents
+    w.host = (data, adj)
+    w.info = {"graph": "exact kNN (K6)", "setup_s": time.time() - t0}
+    log(f"[bench] cfg1 workload ready in {w.info['setup_s']:.1f}s")
+    return w
 
 
-def recall(data, queries, ids, counts, k):
-    from paper_2512_02278_b200 import synth
-    truth = synth.brute_force_gt(data, queries, k)
-    return synth.recall_at_k(ids, counts, truth, k)
+def build_workload(args, rank, ctx, dev, gt_rows=None):
+    return (build_cfg3 if args.workload == "cfg3" else build_cfg1)(args, rank, ctx, dev, gt_rows)
+
+
+def host_index(w):
+    """(vectors n x dim, adjacency n x d) numpy copies of the resident index."""
+    if hasattr(w, "host"):
+        return w.host
+    vec = w.vec[:, :w.centroid.shape[1]].cpu().numpy() if w.vec.shape[1] != w.centroid.shape[1] \
+        else w.vec.cpu().numpy()
+    adj = w.adj.cpu().numpy().view(np.uint32)
+    return vec, adj
+
+
+def workload_config(args, world, rec, w=None, sharded=False):
+    cfg = {
+        "workload": WORKLOADS[args.workload]["desc"],
+        "n": args.n, "dim": args.dim, "degree": args.degree, "queries_per_step_per_gpu": args.nq,
+        "iterations": args.iterations, "beam_width": args.beam, "k": args.k,
+        "entry_count": args.entry, "partitions": 1, "accum": args.accum,
+        "recall_at_10": None if rec is None else round(rec, 4),
+        "recall_sample": args.recall_sample,
+        "l2": ("index and gathers far larger than L2 (38.4 GB vectors, random rows); 256 MiB buffer "
+               "written before every timed step") if args.workload == "cfg3" else
+              "256 MiB buffer written before every timed step",
+        "parallelism": (f"node-sharded x{world}: vectors split by id range, adjacency replicated, "
+                        f"{args.exchange} NVLink peer-store frontier exchange" if sharded
+                        else (f"replicas x{world}" if world > 1 else "single GPU")),
+        "step": ("node-sharded search (ids + dists)" if sharded
+                 else "run_pipeline: assign + route + K1 + combine + hit vectors"),
+    }
+    if w is not None:
+        g = {k: v for k, v in w.info.items() if k not in ("perm",)}
+        if w.graph_sha256:
+            g["adjacency_sha256"] = w.graph_sha256
+        cfg["graph"] = g
+    return cfg
 
 
 # ---------------------------------------------------------------------------
-def reference_arm(args, data, queries, index, nthreads, seconds, min_q=64):
-    """Time the reference's own run_pipeline on a bounded sample."""
+def reference_setup(args):
+    """--impl reference-setup (a separate process): build the workload on the
+    GPU exactly as the dvsg arm does and write the arrays the reference arm
+    needs to args.ref_out; the reference process itself maps no libdvsg."""
+    import torch
+    import paper_2512_02278_b200 as dvs
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    ctx = dvs.Context(0)
+    nq_ref = min(args.nq, 100_000)
+    w = build_workload(args, 0, ctx, dev)
+    vec, adj = host_index(w)
+    out = args.ref_out
+    np.save(os.path.join(out, "vectors.npy"), vec)
+    np.save(os.path.join(out, "adjacency.npy"), adj)
+    np.save(os.path.join(out, "centroid.npy"), w.centroid)
+    np.save(os.path.join(out, "queries.npy"), w.queries[:nq_ref, :args.dim].cpu().numpy())
+    np.save(os.path.join(out, "gt.npy"), w.gt)
+    meta = {"adjacency_sha256": sha256_bytes(adj), "graph": {k: v for k, v in w.info.items()}}
+    with open(os.path.join(out, "meta.json"), "w") as f:
+        json.dump(meta, f)
+    ctx.close()
+
+
+def ref_index(vec, adj, centroid, degree):
+    """The reference's own BuiltIndex over these arrays (oracle/_ref: the
+    unmodified reference sources; compute_entry_order is the reference's)."""
     from oracle.oracle import Oracle, Ref, have_ref
-    kind = "reference" if have_ref() else "port"
-    g = index.graphs[0]
+    n = vec.shape[0]
+    gids = np.arange(n, dtype=np.uint32)
+    if have_ref():
+        return "reference", Ref().index_from_arrays(centroid, np.zeros(1, np.uint32), 1, degree,
+                                                    [(vec, adj, gids)])
+    from paper_2512_02278_b200.api import BuiltIndex, GraphIndex
+    return "port", (Oracle(), BuiltIndex(centroid, np.zeros(1, np.uint32), 1, degree,
+                                         [GraphIndex(vec, gids, degree, adj, None)]))
+
+
+def ref_runner(kind, idx, args, nthreads):
     if kind == "reference":
-        ref = Ref()
-        ridx = ref.index_from_arrays(index.centroids, index.cluster_to_rank, 1, args.degree,
-                                     [(g.vectors, g.adjacency, g.global_ids)])
-
         def run(qs):
-            return ridx.run_pipeline(qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
-                                     nthreads=nthreads, with_vectors=True)
+            return idx.run_pipeline(qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
+                                    nthreads=nthreads, with_vectors=True)
     else:
-        o = Oracle()
+        o, bi = idx
 
         def run(qs):
-            return o.run_pipeline(index, qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
+            return o.run_pipeline(bi, qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
                                   nthreads=nthreads, with_vectors=True)
-    # size the sample so one pass is ~`seconds` of CPU wall time
+    return run
+
+
+def size_sample(run, queries, seconds, nthreads, min_q=64):
     probe = queries[:max(min_q, 2 * nthreads)]
     t0 = time.perf_counter()
     run(probe)
-    dt = time.perf_counter() - t0
-    per_q = dt / probe.shape[0]
-    n = int(min(queries.shape[0], max(probe.shape[0], seconds / max(per_q, 1e-9))))
-    return kind, run, n
-
-
-def cpu_model():
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return "unknown"
+    per_q = (time.perf_counter() - t0) / probe.shape[0]
+    return int(min(queries.shape[0], max(probe.shape[0], seconds / max(per_q, 1e-9))))
 
 
 def run_reference_impl(args, world, rank):
-    """--impl reference: rank 0 times the reference CPU implementation."""
+    """--impl reference: rank 0 times the reference CPU implementation (the
+    graph comes from a separate setup process through /dev/shm)."""
     if rank != 0:
         return
-    import paper_2512_02278_b200 as dvs
-    ctx = dvs.Context(0)  # setup only: builds the shared graph if not cached
-    data, queries, index = workload(args, 0, ctx)
-    ctx.close()
+    t0 = time.time()
+    base = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    out = tempfile.mkdtemp(prefix="dvsg_ref_", dir=base)
+    try:
+        cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference-setup", "--ref-out", out,
+               "--workload", args.workload, "--n", str(args.n), "--nq", str(args.nq), "--dim", str(args.dim),
+               "--rank-latent", str(args.rank_latent), "--degree", str(args.degree),
+               "--probe", str(args.probe), "--cluster-size", str(args.cluster_size),
+               "--k", str(args.k), "--recall-sample", str(args.recall_sample), "--cache", args.cache]
+        env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+        subprocess.run(cmd, check=True, env=env, stdout=sys.stderr)
+        vec = np.load(os.path.join(out, "vectors.npy"), mmap_mode="r")
+        adj = np.load(os.path.join(out, "adjacency.npy"), mmap_mode="r")
+        centroid = np.load(os.path.join(out, "centroid.npy"))
+        queries = np.load(os.path.join(out, "queries.npy"))
+        gt = np.load(os.path.join(out, "gt.npy"))
+        meta = json.load(open(os.path.join(out, "meta.json")))
+        kind, idx = ref_index(vec, adj, centroid, args.degree)
+        del vec, adj
+    finally:
+        shutil.rmtree(out, ignore_errors=True)
+    setup_s = time.time() - t0
     nthreads = os.cpu_count() or 1
-    kind, run, n = reference_arm(args, data, queries, index, nthreads, args.cpu_seconds)
+    run = ref_runner(kind, idx, args, nthreads)
+    n = size_sample(run, queries, args.ref_step_seconds, nthreads)
+    n = max(n, min(gt.shape[0], queries.shape[0]))
     sample = queries[:n]
-    run(sample[: min(n, 4 * nthreads)])  # warm caches / page in the index
+    for _ in range(min(args.warmup, 1)):
+        run(sample[:min(n, 4 * nthreads)])  # page the index in
     times = []
     res = None
     for _ in range(args.steps):
-        t0 = time.perf_counter()
+        t1 = time.perf_counter()
         res = run(sample)
-        times.append(time.perf_counter() - t0)
+        times.append(time.perf_counter() - t1)
     total = sum(times)
     qps = n * args.steps / total
-    rec = recall(data, sample[: min(n, args.recall_sample)], res[0], res[2], args.k)
+    s = min(gt.shape[0], n)
+    rec = recall_at_k(res[0][:s], res[2][:s], gt[:s], args.k)
+    cfg = workload_config(args, world, rec)
+    cfg["graph"] = dict(meta["graph"], adjacency_sha256=meta["adjacency_sha256"])
     line = {
-        "impl": "reference", "metric": "QPS at recall@10>=0.95", "value": qps, "unit": "queries/s",
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, world, rec),
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": nthreads, "kind": kind,
                          "sample": f"{n} of the {args.nq} queries per step, run_pipeline C=1 "
                                    f"(simulator.cpp:245-366) in {nthreads} threads",
-                         "cpu_model": cpu_model()},
+                         "cpu_model": cpu_model(), "setup_s": setup_s},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
 def timeline_summary(dvs, tl, args):
     """Measured copy/compute timeline of the last e2e step:
     validated with check_timeline (simulator.cpp:170-217 rules), with the
@@ -283,197 +485,26 @@ def timeline_summary(dvs, tl, args):
             "lanes": "comm = h2d + d2h on the copy stream, compute = run_pipeline kernels"}
 
 
-def workload_config(args, world, rec):
-    return {
-        "workload": "BASELINE configs[1] at N=1: SIFT-like synthetic 1M x 128 (integer-valued f32, "
-                    "rank-16 latent), exact kNN-32 graph in 1 partition, 100k-query batch per GPU, "
-                    "top-10, beam 64, I=6, entry 64",
-        "n": args.n, "dim": args.dim, "degree": args.degree, "queries_per_step_per_gpu": args.nq,
-        "iterations": args.iterations, "beam_width": args.beam, "k": args.k,
-        "entry_count": args.entry, "partitions": 1, "accum": args.accum,
-        "recall_at_10": None if rec is None else round(rec, 4),
-        "l2": "256 MiB buffer written before every timed step",
-        "parallelism": (f"node-sharded x{world}: vectors split by id range, adjacency replicated, "
-                        f"{args.exchange} NVLink peer-store frontier exchange" if getattr(args, "_sharded", False)
-                        else (f"replicas x{world}" if world > 1 else "single GPU")),
-        "step": ("node-sharded search (ids + dists)" if getattr(args, "_sharded", False)
-                 else "run_pipeline: assign + route + K1 + combine + hit vectors"),
-    }
+class Bufs:
+    def __init__(self, torch, nq, k, dim, dev, vectors=True):
+        self.ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+        self.dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        self.counts = torch.empty((nq,), dtype=torch.int32, device=dev)
+        self.vis = torch.empty((nq,), dtype=torch.int64, device=dev)
+        self.vecs = torch.empty((nq, k, dim), dtype=torch.float32, device=dev) if vectors else None
 
 
-# ---------------------------------------------------------------------------
-def measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries, index, p, ids_ref,
-                    cnt_ref, flush, dev):
-    """K timed steps of the node-sharded search (vectors split across the N
-    GPUs, NVLink frontier exchange, --exchange); ids must equal the replica run's."""
-    from paper_2512_02278_b200.dist import prepare_step, setup_sharded
-    g0 = index.graphs[0]
-    ctx = dvs.Context(local)
-    try:
-        return _measure_sharded(ctx, args, torch, dist, rank, world, data, queries, g0, p, ids_ref,
-                                cnt_ref, flush, dev, setup_sharded, prepare_step)
-    finally:
-        ctx.close()
-
-
-def _measure_sharded(ctx, args, torch, dist, rank, world, data, queries, g0, p, ids_ref, cnt_ref, flush,
-                     dev, setup_sharded, prepare_step):
-    ctx.set_shard_exchange(args.exchange)
-    setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
-    if args.exchange == "nccl":
-        from paper_2512_02278_b200.dist import connect_nccl
-        connect_nccl(ctx, rank)
-    nq, dim, k = args.nq, args.dim, args.k
-    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    d_q = torch.from_numpy(queries).to(dev)
-    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
-    d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
-    d_counts = torch.empty((nq,), dtype=torch.int32, device=dev)
-    d_vis = torch.empty((nq,), dtype=torch.int64, device=dev)
-
-    def run():
-        ctx.search_sharded_device(d_q.data_ptr(), nq, dim, p, d_ids.data_ptr(), d_dists.data_ptr(),
-                                  d_counts.data_ptr(), d_vis.data_ptr())
-
-    for _ in range(max(1, args.warmup)):
-        prepare_step(ctx, dist.barrier)
-        run()
-        ctx.synchronize()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    for i in range(args.steps):
-        flush.fill_(float(i))
-        torch.cuda.synchronize()
-        prepare_step(ctx, dist.barrier)
-        ev0[i].record(stream)
-        run()
-        ev1[i].record(stream)
-        stream.synchronize()
-    t = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    same = torch.tensor([int(np.array_equal(d_ids.cpu().numpy().view(np.uint32), ids_ref) and
-                             np.array_equal(d_counts.cpu().numpy().view(np.uint32), cnt_ref))],
-                        dtype=torch.int32, device=dev)
-    dist.all_reduce(same, op=dist.ReduceOp.MIN)
-    st = ctx.last_search_stats() if args.exchange != "fused" else None
-    tl_sum = None
-    if args.exchange != "fused":
-        # one more (untimed) step with timing on: measured step-kernel vs
-        # barrier / NCCL-exchange intervals on the search stream
-        ctx.set_timing(True)
-        prepare_step(ctx, dist.barrier)
-        run()
-        ctx.synchronize()
-        tl = ctx.last_sharded_timeline(rank)
-        ctx.set_timing(False)
-        if tl:
-            span = max(iv["end"] for iv in tl) - min(iv["start"] for iv in tl)
-            comp = sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == "compute")
-            comm = sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == "comm")
-            tl_sum = {"rank": rank, "intervals": len(tl), "span_ms": span, "step_kernels_ms": comp,
-                      "barrier_or_exchange_ms": comm, "exchange_share": comm / span if span else None}
-    ms = float(t[0])
-    xch = None
-    if st and st["units"]:
-        # bulk protocol, per GPU and step: every remote candidate costs an 8 B
-        # request out and an 8 B key back (a uniform id-range shard makes
-        # (R-1)/R of the visited vectors remote), each query is copied once to
-        # every other rank; HBM side: the same algorithmic bytes as K1
-        vis_q = st["visited"] / st["units"]
-        xbytes = nq * (vis_q * (world - 1) / world * 16 + (world - 1) * 4 * dim)
-        alg = nq * (vis_q * 4 * dim + st["expanded"] / st["units"] * 4 * args.degree + 4 * dim)
-        step_s = ms / args.steps / 1e3
-        xch = {"bytes_per_step_per_gpu": xbytes, "achieved_gbs": xbytes / step_s / 1e9,
-               "nvlink_peak_gbs_per_direction": 900.0, "frac": xbytes / step_s / 1e9 / 900.0,
-               "hbm_alg_gbs_per_gpu": alg / step_s / 1e9, "visited_per_query": vis_q}
-    return {"value": nq * world * args.steps / (ms / 1e3), "unit": "queries/s",
-            "ms_per_step": ms / args.steps, "exchange_roofline": xch, "timeline_rank0": tl_sum,
-            "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; " + (
-                "bulk-synchronous NVLink peer-store frontier exchange (xchg_kernel.cu)" if args.exchange == "bulk"
-                else "bulk protocol, host-driven ncclSend/ncclRecv exchange (baseline)" if args.exchange == "nccl"
-                else "fused NVLink peer-store frontier exchange (shard_kernel.cu)"),
-            "exchange": args.exchange,
-            "ids_identical_to_replica_all_ranks": bool(same[0])}
-
-
-def main():
-    args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference_impl(args, world, rank)
-
-    import torch
-    import paper_2512_02278_b200 as dvs
-
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        # rank 0 must print exactly one JSON line on stdout: keep NCCL's version
-        # banner (NCCL_DEBUG=VERSION/INFO) off stdout
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
-            os.environ["NCCL_DEBUG"] = "WARN"
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    mode = args.mode
-    if mode == "auto":
-        # 1M x 128 (0.64 GB) fits one GPU: replicas are the QPS-optimal layout;
-        # the node-sharded mode is measured beside it at N > 1 (DESIGN.md (e))
-        mode = "replica"
-    sharded = mode == "sharded"
-    args._sharded = sharded
-
-    ctx = dvs.Context(local)
-    data, queries, index = workload(args, rank, ctx)
-    g0 = index.graphs[0]
-    if sharded:
-        from paper_2512_02278_b200.dist import prepare_step, setup_sharded
-        ctx.set_shard_exchange(args.exchange)
-        setup_sharded(ctx, rank, world, data, g0.adjacency, g0.entry_order, g0.global_ids)
-        if args.exchange == "nccl":
-            from paper_2512_02278_b200.dist import connect_nccl
-            connect_nccl(ctx, rank)
-    else:
-        ctx.load_index(index)
-    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
-    nq, dim, k = args.nq, args.dim, args.k
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-
-    d_q = torch.from_numpy(queries).to(dev)
-    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
-    d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
-    d_counts = torch.empty((nq,), dtype=torch.int32, device=dev)
-    d_vecs = torch.empty((nq, k, dim), dtype=torch.float32, device=dev)
-    d_vis = torch.empty((nq,), dtype=torch.int64, device=dev)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
-    torch.cuda.synchronize()
-
-    def pre_step():  # untimed: the sharded arenas must be reset on every rank first
-        if sharded:
-            prepare_step(ctx, dist.barrier if dist else (lambda: None))
-
-    def step():
-        if sharded:
-            ctx.search_sharded_device(d_q.data_ptr(), nq, dim, p, d_ids.data_ptr(),
-                                      d_dists.data_ptr(), d_counts.data_ptr(), d_vis.data_ptr())
-        else:
-            ctx.run_pipeline_device(d_q.data_ptr(), nq, dim, p, 1, d_ids.data_ptr(),
-                                    d_dists.data_ptr(), d_counts.data_ptr(), d_vecs.data_ptr())
-
-    ctx.set_timing(True)
+def timed_steps(args, torch, ctx, stream, step, flush, dist, local, pre_step=lambda: None, stats=True):
+    """W warm-up steps, then K timed steps (CUDA events on the library stream,
+    L2 flushed before each).  -> (total ms, K1 ms, visited, expanded, units,
+    launches, clocks summary)"""
     for _ in range(args.warmup):
         pre_step()
         step()
         ctx.synchronize()
-
-    # ---- timed region: K steps, L2 flushed before each -------------------------
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    k1_ms, vis_tot, exp_tot, units_tot = 0.0, 0, 0, 0
+    k1_ms, vis, exp, units = 0.0, 0, 0, 0
     launches0 = ctx.kernel_launches()
     if dist:
         dist.barrier()
@@ -486,185 +517,357 @@ def main():
             starts[i].record(stream)
             step()
             ends[i].record(stream)
-            st = ctx.last_search_stats()      # syncs the stream
-            k1_ms += ctx.last_timings()["search_ms"]
-            vis_tot += st["visited"]
-            exp_tot += st["expanded"]
-            units_tot += st["units"]
+            if stats:
+                st = ctx.last_search_stats()      # syncs the stream
+                k1_ms += ctx.last_timings()["search_ms"]
+                vis += st["visited"]
+                exp += st["expanded"]
+                units += st["units"]
+            else:
+                stream.synchronize()
         torch.cuda.synchronize()
     launches = ctx.kernel_launches() - launches0
-    step_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t_local = torch.tensor([step_ms, k1_ms], dtype=torch.float64, device=dev)
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t = torch.tensor([ms, k1_ms], dtype=torch.float64, device=flush.device)
     if dist:
         dist.barrier()
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    total_ms, k1_max_ms = float(t_local[0]), float(t_local[1])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0]), float(t[1]), vis, exp, units, launches, clk.summary()
 
-    # ---- parity sample + recall (outside timing) ------------------------------------
-    ids_h = d_ids.cpu().numpy().view(np.uint32)
-    cnt_h = d_counts.cpu().numpy().view(np.uint32)
-    rec = None
-    shard_parity = None
-    if rank == 0:
-        s = min(args.recall_sample, nq)
-        rec = recall(data, queries[:s], ids_h[:s], cnt_h[:s], k)
-        if sharded:  # the sharded traversal must equal the unsharded one exactly
-            ref_ctx = dvs.Context(local)
-            ref_ctx.load_index(index)
-            ri, rd, rc, rv = ref_ctx.beam_search(0, queries[:s], p)
-            vis_h = d_vis.cpu().numpy()[:s]
-            shard_parity = {"queries": s,
-                            "ids_identical": bool(np.array_equal(ri, ids_h[:s]) and np.array_equal(rc, cnt_h[:s])),
-                            "visited_identical": bool(np.array_equal(rv.astype(np.int64), vis_h))}
-            ref_ctx.close()
 
-    # ---- e2e through the public host-buffer call ------------------------------------
-    e2e = None
-    if not args.no_e2e and sharded:
-        # host queries in (pinned H2D), sharded search, ids/dists/counts out (D2H)
-        hq = torch.from_numpy(queries).pin_memory()
-        h_ids = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)
-        h_dists = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
-        h_counts = torch.empty((nq,), dtype=torch.int32, pin_memory=True)
-        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            torch.cuda.synchronize()
-            pre_step()
-            with torch.cuda.stream(stream):
-                ev0[i].record(stream)
-                d_q.copy_(hq, non_blocking=True)
-                step()
-                h_ids.copy_(d_ids, non_blocking=True)
-                h_dists.copy_(d_dists, non_blocking=True)
-                h_counts.copy_(d_counts, non_blocking=True)
-                ev1[i].record(stream)
-            stream.synchronize()
-        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        assert np.array_equal(h_ids.numpy().view(np.uint32), ids_h), "e2e and device paths disagree"
-        e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
-               "h2d_bytes_per_step": int(hq.numel() * 4),
-               "d2h_bytes_per_step": int((h_ids.numel() + h_dists.numel() + h_counts.numel()) * 4),
-               "ms_per_step": float(e_ms[0]) / args.steps,
-               "note": "sharded mode returns ids + dists (hit vectors stay on their owner GPUs)"}
-    elif not args.no_e2e:
-        keep = []
+def e2e_pinned(args, torch, dvs, ctx, w, p, ids_h, cnt_h, flush, dist, world, rank):
+    nq, dim, k = args.nq, args.dim, args.k
+    keep = []
 
-        def pin(shape, dt):
-            t = torch.empty(shape, dtype=dt, pin_memory=True)
-            keep.append(t)
-            return t.numpy()
+    def pin(shape, dt):
+        t = torch.empty(shape, dtype=dt, pin_memory=True)
+        keep.append(t)
+        return t.numpy()
 
-        hq = pin((nq, dim), torch.float32)
-        hq[:] = queries
-        out = {"ids": pin((nq, k), torch.int32).view(np.uint32), "dists": pin((nq, k), torch.float32),
-               "counts": pin((nq,), torch.int32).view(np.uint32), "vectors": pin((nq, k, dim), torch.float32)}
-        ctx.run_pipeline(hq, p, 1, 1, 0, True, out)  # warm
-        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        if dist:
-            dist.barrier()
+    hq = pin((nq, dim), torch.float32)
+    hq[:] = w.queries[:, :dim].cpu().numpy()
+    out = {"ids": pin((nq, k), torch.int32).view(np.uint32), "dists": pin((nq, k), torch.float32),
+           "counts": pin((nq,), torch.int32).view(np.uint32), "vectors": pin((nq, k, dim), torch.float32)}
+    ctx.run_pipeline(hq, p, 1, 1, 0, True, out)  # warm
+    stream = torch.cuda.ExternalStream(ctx.stream, device=flush.device)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))
         torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            torch.cuda.synchronize()
+        ev0[i].record(stream)
+        ctx.run_pipeline(hq, p, 1, 1, 0, True, out)
+        ev1[i].record(stream)
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64,
+                        device=flush.device)
+    if dist:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    assert np.array_equal(out["ids"], ids_h) and np.array_equal(out["counts"], cnt_h), \
+        "host-buffer and device-pointer paths disagree"
+    h2d = hq.nbytes
+    d2h = out["ids"].nbytes + out["dists"].nbytes + out["counts"].nbytes + out["vectors"].nbytes + 4 + 8
+    e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": float(e_ms[0]) / args.steps, "host_buffers": "pinned",
+           "timeline": timeline_summary(dvs, ctx.last_pipeline_timeline(rank), args)}
+    # the drop-in caller of INTEGRATION.md passes ordinary (pageable) memory
+    qp = np.array(hq)
+    outp = {"ids": np.zeros((nq, k), np.uint32), "dists": np.zeros((nq, k), np.float32),
+            "counts": np.zeros(nq, np.uint32), "vectors": np.zeros((nq, k, dim), np.float32)}
+    ctx.run_pipeline(qp, p, 1, 1, 0, True, outp)
+    reps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ctx.run_pipeline(qp, p, 1, 1, 0, True, outp)
+    dt = (time.perf_counter() - t0) / reps
+    e2e["pageable"] = {"value": nq / dt, "unit": "queries/s", "ms_per_step": 1e3 * dt, "steps": reps,
+                       "timing": "host wall clock around dvsg_run_pipeline (synchronous call)",
+                       "ids_identical": bool(np.array_equal(outp["ids"], ids_h))}
+    return e2e
+
+
+def accum_modes(args, torch, dvs, ctx, w, ids_h, cnt_h, dev):
+    """QPS of the same search in the f64 parity mode and the compensated f32
+    mode, and whether their ids equal the headline's (verdict r1 #5)."""
+    nq = args.nq
+    b = Bufs(torch, nq, args.k, args.dim, dev, vectors=False)
+    uq = torch.arange(nq, dtype=torch.int32, device=dev)
+    up = torch.zeros(nq, dtype=torch.int32, device=dev)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    out = {}
+    for mode in ("f64", "f32c"):
+        p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=mode)
+        torch.cuda.synchronize()
+
+        def run():
+            ctx.search_units_device(w.queries.data_ptr(), nq, args.dim, uq.data_ptr(), up.data_ptr(), nq, p,
+                                    b.ids.data_ptr(), b.dists.data_ptr(), b.counts.data_ptr(), b.vis.data_ptr())
+        run()
+        ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        ctx.synchronize()
+        ms = e0.elapsed_time(e1)
+        same = bool(np.array_equal(b.ids.cpu().numpy().view(np.uint32), ids_h) and
+                    np.array_equal(b.counts.cpu().numpy().view(np.uint32), cnt_h))
+        out[mode] = {"value": nq / (ms / 1e3), "unit": "queries/s", "ms_per_search": ms,
+                     "ids_identical_to_headline": same, "step": "K1 search only"}
+    return out
+
+
+def cpu_baseline(args, w, ids_h, cnt_h, dists_h):
+    nthreads = os.cpu_count() or 1
+    t0 = time.time()
+    vec, adj = host_index(w)
+    kind, idx = ref_index(vec, adj, w.centroid, args.degree)
+    if w.graph_sha256 is None:
+        w.graph_sha256 = sha256_bytes(adj)
+    del vec, adj
+    setup_s = time.time() - t0
+    run = ref_runner(kind, idx, args, nthreads)
+    qh = w.queries[:, :args.dim].cpu().numpy()
+    n = size_sample(run, qh, args.cpu_seconds, nthreads)
+    t1 = time.perf_counter()
+    r = run(qh[:n])
+    dt = time.perf_counter() - t1
+    same_ids = np.array_equal(r[0], ids_h[:n]) and np.array_equal(r[2], cnt_h[:n])
+    same_q = int(sum(np.array_equal(r[0][i, :r[2][i]], ids_h[i, :cnt_h[i]]) for i in range(n)))
+    rel = np.abs(r[1] - dists_h[:n]) / np.maximum(np.abs(r[1]), 1e-30)
+    return {"value": n / dt, "unit": "queries/s", "cores": nthreads, "kind": kind,
+            "sample": f"first {n} of the {args.nq} step queries, run_pipeline C=1, {nthreads} threads",
+            "cpu_model": cpu_model(), "ids_identical_to_gpu": bool(same_ids),
+            "queries_identical": same_q, "max_rel_dist_diff": float(rel.max()) if n else None,
+            "setup_s": setup_s}
+
+
+# ---------------------------------------------------------------------------
+def sharded_measure(args, torch, dvs, dist, ctx, w, rank, world, local, flush, ids_ref, cnt_ref, dev):
+    """K timed steps of the node-sharded search (this rank keeps 1/N of the
+    vectors; NVLink frontier exchange); ids must equal the replica run's."""
+    from paper_2512_02278_b200.dist import connect_nccl, prepare_step, setup_sharded_resident
+    ctx.set_shard_exchange(args.exchange)
+    setup_sharded_resident(ctx, rank, world)
+    if args.exchange == "nccl":
+        connect_nccl(ctx, rank)
+    nq, dim = args.nq, args.dim
+    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+    b = Bufs(torch, nq, args.k, dim, dev, vectors=False)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def step():
+        ctx.search_sharded_device(w.queries.data_ptr(), nq, dim, p, b.ids.data_ptr(), b.dists.data_ptr(),
+                                  b.counts.data_ptr(), b.vis.data_ptr())
+
+    ms, _, _, _, _, launches, clk = timed_steps(args, torch, ctx, stream, step, flush, dist, local,
+                                                pre_step=lambda: prepare_step(ctx, dist.barrier), stats=False)
+    st = ctx.last_search_stats() if args.exchange != "fused" else None
+    same = torch.tensor([int(np.array_equal(b.ids.cpu().numpy().view(np.uint32), ids_ref) and
+                             np.array_equal(b.counts.cpu().numpy().view(np.uint32), cnt_ref))],
+                        dtype=torch.int32, device=dev)
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    tl_sum = None
+    if args.exchange != "fused":
+        ctx.set_timing(True)
+        prepare_step(ctx, dist.barrier)
+        step()
+        ctx.synchronize()
+        tl = ctx.last_sharded_timeline(rank)
+        ctx.set_timing(False)
+        if tl:
+            span = max(iv["end"] for iv in tl) - min(iv["start"] for iv in tl)
+            comp = sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == "compute")
+            comm = sum(iv["end"] - iv["start"] for iv in tl if iv["lane"] == "comm")
+            tl_sum = {"rank": rank, "intervals": len(tl), "span_ms": span, "step_kernels_ms": comp,
+                      "barrier_or_exchange_ms": comm, "exchange_share": comm / span if span else None}
+    # e2e through the public call: pinned host queries in, ids / dists / counts out
+    hq = torch.from_numpy(w.queries[:, :dim].cpu().numpy()).pin_memory()
+    h_ids = torch.empty((nq, args.k), dtype=torch.int32, pin_memory=True)
+    h_dists = torch.empty((nq, args.k), dtype=torch.float32, pin_memory=True)
+    h_counts = torch.empty((nq,), dtype=torch.int32, pin_memory=True)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dq = torch.empty_like(w.queries)
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        prepare_step(ctx, dist.barrier)
+        with torch.cuda.stream(stream):
             ev0[i].record(stream)
-            ctx.run_pipeline(hq, p, 1, 1, 0, True, out)
+            dq.copy_(hq, non_blocking=True)
+            ctx.search_sharded_device(dq.data_ptr(), nq, dim, p, b.ids.data_ptr(), b.dists.data_ptr(),
+                                      b.counts.data_ptr(), b.vis.data_ptr())
+            h_ids.copy_(b.ids, non_blocking=True)
+            h_dists.copy_(b.dists, non_blocking=True)
+            h_counts.copy_(b.counts, non_blocking=True)
             ev1[i].record(stream)
-        torch.cuda.synchronize()
-        e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        assert np.array_equal(out["ids"], ids_h) and np.array_equal(out["counts"], cnt_h), \
-            "host-buffer and device-pointer paths disagree"
-        h2d = hq.nbytes
-        d2h = out["ids"].nbytes + out["dists"].nbytes + out["counts"].nbytes + out["vectors"].nbytes + 4 + 8
-        e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": float(e_ms[0]) / args.steps,
-               "timeline": timeline_summary(dvs, ctx.last_pipeline_timeline(rank), args)}
+        stream.synchronize()
+    e_ms = torch.tensor([sum(a.elapsed_time(c) for a, c in zip(ev0, ev1))], dtype=torch.float64, device=dev)
+    dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
+           "h2d_bytes_per_step": int(hq.numel() * 4),
+           "d2h_bytes_per_step": int((h_ids.numel() + h_dists.numel() + h_counts.numel()) * 4),
+           "ms_per_step": float(e_ms[0]) / args.steps, "host_buffers": "pinned",
+           "ids_identical": bool(np.array_equal(h_ids.numpy().view(np.uint32), ids_ref)),
+           "note": "sharded mode returns ids + dists (hit vectors stay on their owner GPUs)"}
+    xch = None
+    if st and st["units"]:
+        vis_q = st["visited"] / st["units"]
+        dpad = (dim + 3) // 4 * 4
+        xbytes = nq * (vis_q * (world - 1) / world * 16 + (world - 1) * 4 * dim)
+        alg = nq * (vis_q * 4 * dpad + st["expanded"] / st["units"] * 4 * args.degree + 4 * dpad)
+        step_s = ms / args.steps / 1e3
+        xch = {"bytes_per_step_per_gpu": xbytes, "achieved_gbs": xbytes / step_s / 1e9,
+               "nvlink_peak_gbs_per_direction": 900.0, "frac": xbytes / step_s / 1e9 / 900.0,
+               "hbm_alg_gbs_per_gpu": alg / step_s / 1e9, "visited_per_query": vis_q}
+    return {"value": nq * world * args.steps / (ms / 1e3), "unit": "queries/s",
+            "ms_per_step": ms / args.steps, "exchange_roofline": xch, "timeline_rank0": tl_sum,
+            "gpu_launches": int(launches), "clocks": clk,
+            "layout": f"vectors node-sharded {world} ways (id ranges), adjacency replicated; " + (
+                "bulk-synchronous NVLink peer-store frontier exchange (xchg_kernel.cu)" if args.exchange == "bulk"
+                else "bulk protocol, host-driven ncclSend/ncclRecv exchange (baseline)" if args.exchange == "nccl"
+                else "fused NVLink peer-store frontier exchange (shard_kernel.cu)"),
+            "exchange": args.exchange, "ids_identical_to_replica_all_ranks": bool(same[0]), "e2e": e2e}
 
-    # ---- node-sharded mode beside the replica headline (N > 1) -------------------------
-    sharded_side = None
-    if world > 1 and not sharded and args.mode == "auto":
-        # side measurements must not cost the headline line: a failure (raised
-        # on every rank alike, e.g. out of memory) is reported in the JSON
-        try:
-            sharded_side = measure_sharded(args, dvs, torch, dist, local, rank, world, data, queries,
-                                           index, p, ids_h, cnt_h, flush, dev)
-        except Exception as e:  # noqa: BLE001
-            sharded_side = {"error": f"{type(e).__name__}: {e}"}
-        if "error" not in sharded_side and args.exchange != "nccl" and not args.no_nccl_baseline:
-            # the same protocol over host-driven NCCL send/recv: the measured baseline
-            ex = args.exchange
-            args.exchange = "nccl"
-            try:
-                sharded_side["nccl_baseline"] = measure_sharded(
-                    args, dvs, torch, dist, local, rank, world, data, queries, index, p, ids_h, cnt_h,
-                    flush, dev)
-            except Exception as e:  # noqa: BLE001
-                sharded_side["nccl_baseline"] = {"error": f"{type(e).__name__}: {e}"}
-            finally:
-                args.exchange = ex
 
-    # ---- CPU baseline (rank 0, N=1) ---------------------------------------------------
+def self_launch(args):
+    """`--gpus N` without torchrun: relaunch this command under torchrun."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def main():
+    args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.impl == "reference-setup":
+        return reference_setup(args)
+    if env_world is None and args.gpus > 1 and args.impl == "dvsg":
+        sys.exit(self_launch(args))
+    world = int(env_world or "1")
+    if args.impl == "dvsg" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_impl(args, world, rank)
+
+    import torch
+    import paper_2512_02278_b200 as dvs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        # rank 0 must print exactly one JSON line on stdout: keep NCCL's banner off stdout
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):
+            os.environ["NCCL_DEBUG"] = "WARN"
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    sharded = world > 1 and args.mode in ("auto", "sharded")
+
+    ctx = dvs.Context(local)
+    w = build_workload(args, rank, ctx, dev)
+    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+    nq, dim, k = args.nq, args.dim, args.k
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    b = Bufs(torch, nq, k, dim, dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.run_pipeline_device(w.queries.data_ptr(), nq, dim, p, 1, b.ids.data_ptr(), b.dists.data_ptr(),
+                                b.counts.data_ptr(), b.vecs.data_ptr())
+
+    # ---- the replica / single-GPU run_pipeline (headline at N = 1) ----------------
+    ctx.set_timing(True)
+    total_ms, k1_ms, vis_tot, exp_tot, units_tot, launches, clocks = timed_steps(
+        args, torch, ctx, stream, step, flush, dist, local)
+    ctx.set_timing(False)
+    ids_h = b.ids.cpu().numpy().view(np.uint32)
+    cnt_h = b.counts.cpu().numpy().view(np.uint32)
+    dists_h = b.dists.cpu().numpy()
+    s = w.gt.shape[0]
+    rec = recall_at_k(ids_h[:s], cnt_h[:s], w.gt, k)
+    replica = {"value": nq * world * args.steps / (total_ms / 1e3), "unit": "queries/s",
+               "ms_per_step": total_ms / args.steps, "recall_at_10": round(rec, 4)}
+
+    ctx.set_timing(True)  # per-microbatch events of the e2e pipeline (measured timeline)
+    e2e = None if args.no_e2e or sharded else e2e_pinned(args, torch, dvs, ctx, w, p, ids_h, cnt_h, flush,
+                                                         dist, world, rank)
+    ctx.set_timing(False)
+    modes = None if args.no_modes or sharded else accum_modes(args, torch, dvs, ctx, w, ids_h, cnt_h, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            nthreads = os.cpu_count() or 1
-            kind, run, n = reference_arm(args, data, queries, index, nthreads, args.cpu_seconds)
-            t0 = time.perf_counter()
-            r = run(queries[:n])
-            dt = time.perf_counter() - t0
-            same = np.array_equal(r[0], ids_h[:n]) and np.array_equal(r[2], cnt_h[:n])
-            cpu = {"value": n / dt, "unit": "queries/s", "cores": nthreads, "kind": kind,
-                   "sample": f"first {n} of the {nq} step queries, run_pipeline C=1, {nthreads} threads",
-                   "cpu_model": cpu_model(), "ids_identical_to_gpu": bool(same)}
+            cpu = cpu_baseline(args, w, ids_h, cnt_h, dists_h)
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "unavailable",
-                   "sample": f"failed: {ex}"}
+                   "sample": f"failed: {type(ex).__name__}: {ex}"}
+    elif rank == 0 and args.workload == "cfg3" and w.graph_sha256 is None:
+        w.graph_sha256 = sha256_bytes(w.adj.cpu().numpy())
+
+    # ---- N > 1: the node-sharded north-star layout is the headline ------------------
+    shard = None
+    if sharded:
+        try:
+            shard = sharded_measure(args, torch, dvs, dist, ctx, w, rank, world, local, flush, ids_h, cnt_h, dev)
+        except Exception as ex:  # noqa: BLE001
+            shard = {"error": f"{type(ex).__name__}: {ex}"}
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
     peak, peak_kind = peaks()
-    d4 = 4 * dim
-    alg_bytes = vis_tot * d4 + exp_tot * 4 * args.degree + units_tot * d4
-    achieved = alg_bytes / args.steps / (k1_max_ms / args.steps / 1e3) / 1e9
-    traffic = None
+    dpad = (dim + 3) // 4 * 4
+    alg_bytes = vis_tot * 4 * dpad + exp_tot * 4 * args.degree + units_tot * 4 * dpad
+    achieved = alg_bytes / args.steps / (k1_ms / args.steps / 1e3) / 1e9
+    traffic, tsrc = None, None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    key = f"{args.workload}_n{args.n}_q{nq}_w{args.beam}_I{args.iterations}_{args.accum}"
     if os.path.isfile(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("config_key") == f"n{args.n}_q{nq}_w{args.beam}_I{args.iterations}_{args.accum}":
-                traffic = tj.get("dram_bytes_per_launch")
+            ent = tj.get(key) if isinstance(tj, dict) else None
+            if ent:
+                traffic, tsrc = ent.get("dram_bytes_per_launch"), ent.get("source")
         except Exception:
             traffic = None
-    value = nq * world * args.steps / (total_ms / 1e3)
+    headline = shard if (sharded and shard and "error" not in shard) else None
+    value = headline["value"] if headline else nq * world * args.steps / (total_ms / 1e3)
+    ms_step = headline["ms_per_step"] if headline else total_ms / args.steps
+    eff_accum = args.accum if args.accum != "f32" or ctx.index_integral() else "f64/f32c (upgraded)"
     line = {
-        "metric": "QPS at recall@10>=0.95", "value": value, "unit": "queries/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": workload_config(args, world, rec),
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": eff_accum, "data": "synthetic",
+        "config": workload_config(args, world, rec, w, sharded=bool(headline)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": ("dvsg::search_kernel (K1)" if not getattr(args, "_sharded", False) else
-                                ("dvsg::xg_step (bulk exchange)" if args.exchange == "bulk"
-                                 else "dvsg::xg_step (bulk protocol, NCCL exchange)" if args.exchange == "nccl"
-                                 else "dvsg::search_sharded_kernel (fused exchange)")),
-                     "k1_ms_per_step": k1_max_ms / args.steps,
-                     "alg_bytes_per_step": alg_bytes / args.steps,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
+                     "peak_kind": peak_kind, "kernel": "dvsg::search_kernel (K1)",
+                     "k1_ms_per_step": k1_ms / args.steps, "alg_bytes_per_step": alg_bytes / args.steps,
                      "visited_per_query": vis_tot / max(units_tot, 1),
-                     "expanded_per_query": exp_tot / max(units_tot, 1)},
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "sharded_parity_vs_unsharded": shard_parity,
-        "sharded_mode": sharded_side,
-        "clocks": clk.summary(),
+                     "expanded_per_query": exp_tot / max(units_tot, 1),
+                     "k1_share_of_step": k1_ms / total_ms if total_ms else None},
+        "cpu_baseline": cpu, "e2e": headline["e2e"] if headline else e2e, "gpu_launches": int(headline["gpu_launches"] if headline else launches),
+        "accum_modes": modes,
+        "clocks": headline["clocks"] if headline else clocks,
     }
+    if world > 1:
+        line["replicas"] = replica
+        line["sharded_mode"] = shard
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

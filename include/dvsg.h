@@ -151,6 +151,11 @@ dvsg_status dvsg_beam_search_sharded_emulated(dvsg_ctx *ctx, int nranks, const f
 dvsg_status dvsg_shard_init(dvsg_ctx *ctx, int nranks, int rank, uint64_t n_total, int dim,
                             int out_degree, const float *shard_vectors, const uint32_t *adjacency,
                             const uint32_t *global_ids, const uint32_t *entry_order);
+/* Same, from the context's one resident partition (e.g. built on the
+ * device with dvsg_partition_alloc_device): every rank builds or loads the
+ * whole graph, then keeps only its shard rows of the vectors -- no host copy
+ * of a 50 GB index. */
+dvsg_status dvsg_shard_init_resident(dvsg_ctx *ctx, int nranks, int rank);
 /* 64-byte IPC handle of this rank's comm arena (exchange it across ranks). */
 dvsg_status dvsg_shard_export(dvsg_ctx *ctx, void *handle_out);
 /* Open every rank's arena (handles: nranks x 64 bytes, in rank order). */

@@ -64,6 +64,7 @@ _SIGS = {
                                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "dvsg_shard_init": (c_int, [c_void_p, c_int, c_int, c_uint64, c_int, c_int, c_void_p, c_void_p,
                                 c_void_p, c_void_p]),
+    "dvsg_shard_init_resident": (c_int, [c_void_p, c_int, c_int]),
     "dvsg_shard_export": (c_int, [c_void_p, c_void_p]),
     "dvsg_shard_connect": (c_int, [c_void_p, c_void_p]),
     "dvsg_shard_prepare": (c_int, [c_void_p]),

@@ -274,6 +274,10 @@ class Context:
         check(lib.dvsg_shard_init(self._h, int(nranks), int(rank), int(n_total), v.shape[1],
                                   int(adj.shape[1]), _ptr(v), _ptr(adj), _ptr(gids), _ptr(eo)))
 
+    def shard_init_resident(self, nranks: int, rank: int) -> None:
+        """dvsg_shard_init_resident: keep this rank's rows of the resident partition."""
+        check(lib.dvsg_shard_init_resident(self._h, int(nranks), int(rank)))
+
     def shard_export(self) -> bytes:
         buf = ctypes.create_string_buffer(64)
         check(lib.dvsg_shard_export(self._h, buf))

@@ -1438,6 +1438,10 @@ dvsg_status dvsg_beam_search_sharded_emulated(dvsg_ctx* c, int nranks, const flo
   });
 }
 
+namespace {
+void shard_arena_setup(dvsg_ctx* c, int nranks, int rank, uint64_t n_total);
+}
+
 dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total, int dim, int out_degree,
                             const float* shard_vectors, const uint32_t* adjacency,
                             const uint32_t* global_ids, const uint32_t* entry_order) {
@@ -1482,26 +1486,62 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
     c->part_mono.push_back(global_ids ? ids_increasing(global_ids, n_total) : 1);
     c->all_integral = integral_all(shard_vectors, (hi - lo) * (uint64_t)dim);
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
-    auto& sh = c->sh;
-    if (sh.arena) cudaFree(sh.arena);
-    sh = dvsg_ctx::Shard{};
-    sh.active = true;
-    sh.nranks = nranks;
-    sh.rank = rank;
-    sh.n_total = n_total;
-    sh.shard_rows = S;
-    sh.gpr_max = 8 * c->num_sms;
-    sh.ring_cap = (uint32_t)pow2_at_least((uint64_t)nranks * sh.gpr_max);
-    sh.arena_bytes = shard_arena_bytes(nranks, sh.gpr_max, sh.ring_cap, c->dpad);
-    // + the bulk-exchange region (queries, inboxes, replies of one wave)
-    sh.xg_off = (sh.arena_bytes + 4095) & ~(size_t)4095;
-    sh.xg_bytes = (size_t)env_u64("DVSG_XG_ARENA_MB", 16384) << 20;
-    sh.arena_bytes = sh.xg_off + sh.xg_bytes;
-    cuda_check(cudaMalloc(&sh.arena, sh.arena_bytes), "arena");
-    cuda_check(cudaMemset(sh.arena, 0, sh.xg_off + kXgHeader), "arena reset");
-    for (auto& e : c->xg.epoch) e = 0;
+    shard_arena_setup(c, nranks, rank, n_total);
   });
 }
+
+dvsg_status dvsg_shard_init_resident(dvsg_ctx* c, int nranks, int rank) {
+  return guarded([&] {
+    set_device(c);
+    if (nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) fail(DVSG_EINVAL, "shard_init: rank %d of %d", rank, nranks);
+    if (c->sh.active) fail(DVSG_EINVAL, "shard_init_resident: already sharded");
+    if (c->parts.size() != 1 || c->parts[0].row_off != 0) fail(DVSG_EINVAL, "shard_init_resident: needs exactly one resident partition");
+    if (c->dim > 768) fail(DVSG_EINVAL, "shard_init: dim %d outside 1..768", c->dim);
+    const uint64_t n_total = c->parts[0].n;
+    const uint64_t S = (n_total + (uint64_t)nranks - 1) / (uint64_t)nranks;
+    const uint64_t lo = std::min<uint64_t>(n_total, S * (uint64_t)rank);
+    const uint64_t hi = std::min<uint64_t>(n_total, lo + S);
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    // keep only this rank's rows of the vectors; adjacency, global ids and
+    // entry order stay whole (replicated)
+    const uint64_t rows = std::max<uint64_t>(hi - lo, 1);
+    DevBuf<float> own;
+    own.reserve(rows * (uint64_t)c->dpad, c->stream);
+    cuda_check(cudaMemset(own.p, 0, rows * (uint64_t)c->dpad * 4), "memset");
+    if (hi > lo)
+      cuda_check(cudaMemcpy(own.p, c->vec.p + lo * c->dpad, (hi - lo) * (uint64_t)c->dpad * 4, cudaMemcpyDeviceToDevice), "shard rows");
+    std::swap(c->vec.p, own.p);
+    std::swap(c->vec.cap, own.cap);
+    c->parts[0].cluster = 0;
+    c->rows = n_total;
+    c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
+    shard_arena_setup(c, nranks, rank, n_total);
+  });
+}
+
+namespace {
+void shard_arena_setup(dvsg_ctx* c, int nranks, int rank, uint64_t n_total) {
+  const uint64_t S = (n_total + (uint64_t)nranks - 1) / (uint64_t)nranks;
+  auto& sh = c->sh;
+  if (sh.arena) cudaFree(sh.arena);
+  sh = dvsg_ctx::Shard{};
+  sh.active = true;
+  sh.nranks = nranks;
+  sh.rank = rank;
+  sh.n_total = n_total;
+  sh.shard_rows = S;
+  sh.gpr_max = 8 * c->num_sms;
+  sh.ring_cap = (uint32_t)pow2_at_least((uint64_t)nranks * sh.gpr_max);
+  sh.arena_bytes = shard_arena_bytes(nranks, sh.gpr_max, sh.ring_cap, c->dpad);
+  // + the bulk-exchange region (queries, inboxes, replies of one wave)
+  sh.xg_off = (sh.arena_bytes + 4095) & ~(size_t)4095;
+  sh.xg_bytes = (size_t)env_u64("DVSG_XG_ARENA_MB", 16384) << 20;
+  sh.arena_bytes = sh.xg_off + sh.xg_bytes;
+  cuda_check(cudaMalloc(&sh.arena, sh.arena_bytes), "arena");
+  cuda_check(cudaMemset(sh.arena, 0, sh.xg_off + kXgHeader), "arena reset");
+  for (auto& e : c->xg.epoch) e = 0;
+}
+}  // namespace
 
 dvsg_status dvsg_shard_export(dvsg_ctx* c, void* handle_out) {
   return guarded([&] {

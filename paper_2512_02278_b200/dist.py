@@ -56,6 +56,15 @@ def setup_sharded(ctx, rank: int, nranks: int, data, adjacency, entry_order,
     return lo, hi
 
 
+def setup_sharded_resident(ctx, rank: int, nranks: int, group=None,
+                           exchange=exchange_handles) -> None:
+    """Shard the context's resident partition (every rank built the same
+    graph) and connect to every rank's comm arena."""
+    ctx.shard_init_resident(nranks, rank)
+    handles = exchange(ctx.shard_export(), group)
+    ctx.shard_connect(handles)
+
+
 def connect_nccl(ctx, rank: int, group=None) -> None:
     """NCCL communicator for the 'nccl' exchange: rank 0's unique id is
     broadcast over torch.distributed (control plane only)."""

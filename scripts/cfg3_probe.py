@@ -29,10 +29,12 @@ def main():
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--nq", type=int, default=100_000)
     ap.add_argument("--gt", type=int, default=2000)
-    ap.add_argument("--cluster-size", type=int, default=1536)
+    ap.add_argument("--cluster-size", type=int, default=1024)
     ap.add_argument("--probe", type=int, default=8)
     ap.add_argument("--sweep", default="6x64,8x64,10x64,8x96,10x96,12x96,10x128,12x128")
     ap.add_argument("--accum", default="f32")
+    ap.add_argument("--keep", type=int, default=16)
+    ap.add_argument("--no-optimize", action="store_true")
     args = ap.parse_args()
     dev = "cuda:0"
     ctx = dvs.Context(0)
@@ -41,7 +43,7 @@ def main():
     torch.cuda.synchronize()
     log(f"[probe] data {args.n}x{args.dim} in {time.time() - t0:.1f}s")
     info = ivf.build_graph_ivf(ctx, x, degree=32, cluster_size=args.cluster_size, probe=args.probe,
-                               dim=args.dim, log=log)
+                               dim=args.dim, optimize=not args.no_optimize, keep=args.keep, log=log)
     del x
     torch.cuda.empty_cache()
     pv, pa, pg, pe, n = ctx.partition_view_device(0)
@@ -87,7 +89,7 @@ def main():
         alg = (vis * 4 * dpad + it * w * 128 + 4 * dpad) * nq
         line = {"n": args.n, "dim": args.dim, "iters": it, "beam": w, "recall@10": round(float(rec), 4),
                 "qps": nq / (ms / 1e3), "ms": ms, "visited": vis, "alg_gbs": alg / (ms / 1e3) / 1e9,
-                "accum": args.accum, "build": {k2: v for k2, v in info.items() if k2 != "perm"}}
+                "accum": args.accum, "keep": args.keep, "build": {k2: v for k2, v in info.items() if k2 != "perm"}}
         print(json.dumps(line), flush=True)
         log(f"[probe] I={it} w={w}: recall {rec:.4f}, {nq / (ms / 1e3):,.0f} QPS, visited {vis:.0f}")
     ctx.close()
