@@ -9,7 +9,7 @@ Workloads (BASELINE.json configs):
         100M x 96 (integer-valued f32, rank-16 latent), degree-32 graph built
         on the GPU (cluster-restricted kNN + CAGRA-style rank pruning and
         reverse edges, paper_2512_02278_b200/ivf.py), 1M-query batch per GPU
-        per step, top-10, beam 64, I=10, entry 64 (calibrated: recall@10
+        per step, top-10, beam 16, I=24, entry 16 (calibrated: recall@10
         >= 0.95 against brute-force ground truth on a 2,000-query sample).
   cfg1 -- configs[1] at N=1: 1M x 128, exact kNN-32 graph, 100k queries, I=6.
 
@@ -60,12 +60,12 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only without MEASU
 METRIC = "QPS at recall@10>=0.95"
 
 WORKLOADS = {
-    "cfg3": dict(n=100_000_000, dim=96, nq=1_000_000, iterations=10, beam=64, entry=64, k=10, degree=32,
+    "cfg3": dict(n=100_000_000, dim=96, nq=1_000_000, iterations=24, beam=16, entry=16, k=10, degree=32,
                  graph="ivf",
                  desc="BASELINE configs[2]: Deep-like synthetic 100M x 96 (integer-valued f32, rank-16 "
                       "latent), degree-32 graph (GPU-built: cluster-restricted kNN + CAGRA-style rank "
-                      "pruning / reverse edges) in 1 partition, 1M-query batch per GPU, top-10, beam 64, "
-                      "I=10, entry 64"),
+                      "pruning / reverse edges) in 1 partition, 1M-query batch per GPU, top-10, beam 16, "
+                      "I=24, entry 16"),
     "cfg1": dict(n=1_000_000, dim=128, nq=100_000, iterations=6, beam=64, entry=64, k=10, degree=32,
                  graph="exact",
                  desc="BASELINE configs[1] at N=1: SIFT-like synthetic 1M x 128 (integer-valued f32, "
@@ -93,6 +93,8 @@ def parse(argv=None):
     ap.add_argument("--accum", choices=["f32", "f64", "f32c"], default="f32")
     ap.add_argument("--probe", type=int, default=8, help="cfg3 graph build: clusters probed per row")
     ap.add_argument("--cluster-size", type=int, default=1024, help="cfg3 graph build: rows per cluster")
+    ap.add_argument("--keep", type=int, default=12,
+                    help="cfg3 graph build: pruned forward edges per row (the rest are reverse edges)")
     ap.add_argument("--recall-sample", type=int, default=2000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=5.0,
@@ -232,7 +234,7 @@ def build_cfg3(args, rank, ctx, dev, gt_rows=None):
     dpad = (args.dim + 3) // 4 * 4
     x = ivf.sift_like_device(args.n, args.dim, args.rank_latent, seed=1, device=dev, dpad=dpad)
     info = ivf.build_graph_ivf(ctx, x, degree=args.degree, cluster_size=args.cluster_size, probe=args.probe,
-                               dim=args.dim, optimize=True, log=log)
+                               dim=args.dim, optimize=True, keep=args.keep, log=log)
     del x
     info.pop("perm")
     torch.cuda.empty_cache()
@@ -408,7 +410,7 @@ def run_reference_impl(args, world, rank):
         cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference-setup", "--ref-out", out,
                "--workload", args.workload, "--n", str(args.n), "--nq", str(args.nq), "--dim", str(args.dim),
                "--rank-latent", str(args.rank_latent), "--degree", str(args.degree),
-               "--probe", str(args.probe), "--cluster-size", str(args.cluster_size),
+               "--probe", str(args.probe), "--cluster-size", str(args.cluster_size), "--keep", str(args.keep),
                "--k", str(args.k), "--recall-sample", str(args.recall_sample), "--cache", args.cache]
         env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
         subprocess.run(cmd, check=True, env=env, stdout=sys.stderr)

@@ -66,8 +66,10 @@ def main():
     up = torch.zeros(nq, dtype=torch.int32, device=dev)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     for s in args.sweep.split(","):
-        it, w = (int(v) for v in s.split("x"))
-        p = dvs.SearchParams(it, w, k, w, accum=args.accum)
+        parts = [int(v) for v in s.split("x")]
+        it, w = parts[0], parts[1]
+        ent = parts[2] if len(parts) > 2 else w
+        p = dvs.SearchParams(it, w, k, ent, accum=args.accum)
         torch.cuda.synchronize()
 
         def run():
@@ -87,11 +89,11 @@ def main():
         rec = np.mean([len(set(ids[i, :cnt[i]].tolist()) & set(gt[i].tolist())) / 10 for i in range(args.gt)])
         vis = float(d_vis.double().mean())
         alg = (vis * 4 * dpad + it * w * 128 + 4 * dpad) * nq
-        line = {"n": args.n, "dim": args.dim, "iters": it, "beam": w, "recall@10": round(float(rec), 4),
+        line = {"n": args.n, "dim": args.dim, "iters": it, "beam": w, "entry": ent, "recall@10": round(float(rec), 4),
                 "qps": nq / (ms / 1e3), "ms": ms, "visited": vis, "alg_gbs": alg / (ms / 1e3) / 1e9,
                 "accum": args.accum, "keep": args.keep, "build": {k2: v for k2, v in info.items() if k2 != "perm"}}
         print(json.dumps(line), flush=True)
-        log(f"[probe] I={it} w={w}: recall {rec:.4f}, {nq / (ms / 1e3):,.0f} QPS, visited {vis:.0f}")
+        log(f"[probe] I={it} w={w} E={ent}: recall {rec:.4f}, {nq / (ms / 1e3):,.0f} QPS, visited {vis:.0f}")
     ctx.close()
 
 
