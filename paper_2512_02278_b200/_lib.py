@@ -11,7 +11,8 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int, c_uint32, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdvsg.so")
+# DVSG_LIB selects a build variant (scripts/build_variant.sh) for A/B measurements
+LIB_PATH = os.environ.get("DVSG_LIB") or os.path.join(_HERE, "libdvsg.so")
 
 if not os.path.isfile(LIB_PATH):
     raise ImportError(

@@ -6,7 +6,10 @@
 
 namespace dvsg {
 
-constexpr int kThreads = 256;        // K1 CTA size (8 warps)
+#ifndef DVSG_K1_THREADS
+#define DVSG_K1_THREADS 256
+#endif
+constexpr int kThreads = DVSG_K1_THREADS;  // K1 CTA size (8 warps; build variants may change it)
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
@@ -157,7 +160,7 @@ cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sm
                           int max_grid, cudaStream_t stream, int* grid_out);
 // Shared-memory bytes K1 needs for these args (hash in smem when hash_global==nullptr).
 size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_smem);
-constexpr int kChunk = 2048;  // raw candidates per dedup/score/merge chunk (8 per thread)
+constexpr int kChunk = 8 * kThreads;  // raw candidates per dedup/score/merge chunk (8 per thread)
 
 // K5 assign (route_kernels.cu): nq x c cluster ids, exact fp64 expanded form.
 // scratch: nq x (clusters + 1) u64 (keys + query norms of the tiled large-C path).
