@@ -172,9 +172,10 @@ cudaError_t launch_combine(uint64_t nq, int nparts, const uint32_t* ids, const f
                            const uint32_t* counts, int stride, int k, uint32_t* out_ids,
                            float* out_dists, uint32_t* out_count, int* err_flag,
                            cudaStream_t stream);
-// Route: build (unit_query, unit_part) from the assignment and the cluster->slot map.
+// Route: build (unit_query, unit_part) from the assignment and the cluster->slot map
+// (nmap entries); an id >= nmap or a non-resident cluster sets bit 0 of *err_flag.
 cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,
-                         const int32_t* cluster_to_slot, uint32_t* unit_query,
+                         const int32_t* cluster_to_slot, uint32_t nmap, uint32_t* unit_query,
                          uint32_t* unit_part, int* err_flag, cudaStream_t stream);
 // Attach hit vectors (simulator.cpp:329-333): gid -> (slot row) locator.
 cudaError_t launch_gather_vectors(const uint32_t* ids, const uint32_t* counts, uint64_t nq,

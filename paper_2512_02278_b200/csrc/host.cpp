@@ -153,6 +153,7 @@ struct dvsg_ctx {
   DevBuf<float> d_cents;
   DevBuf<double> d_cent_norms;
   DevBuf<int32_t> d_cluster_slot;
+  uint32_t slot_map_n = 0;
   bool slot_dirty = true;
   DevBuf<uint64_t> d_locator;
   uint64_t locator_n = 0;
@@ -256,6 +257,7 @@ void sync_slots(dvsg_ctx* c) {
   for (size_t i = 0; i < c->parts.size(); ++i) m[c->parts[i].cluster] = (int32_t)i;
   c->d_cluster_slot.reserve(m.size(), c->stream);
   cuda_check(cudaMemcpyAsync(c->d_cluster_slot.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice, c->stream), "slots");
+  c->slot_map_n = (uint32_t)m.size();
   cuda_check(cudaStreamSynchronize(c->stream), "sync slots");
   c->slot_dirty = false;
 }
@@ -353,6 +355,12 @@ K1Shape k1_shape(dvsg_ctx* c, const dvsg_search_params* p, uint64_t nmax, bool a
   const uint64_t entries = std::min<uint64_t>((uint64_t)p->entry_count, nmax);
   const uint64_t bound = std::min<uint64_t>(nmax, entries + (uint64_t)p->iterations * (uint64_t)p->beam_width * (uint64_t)c->dg);
   k.hsize = std::max<uint64_t>(64, pow2_at_least(bound + 1));
+  // linear probing near 100% load costs hundreds of probes per insert.  When
+  // the partition size is the bound (a small partition can be explored
+  // completely) keep the worst case at <= 3/4 load.  The I*w*dg bound is
+  // never reached in practice (duplicate neighbours), and doubling those
+  // tables would push the per-CTA regions out of L2.
+  if (bound == nmax && 4 * (bound + 1) > 3 * k.hsize) k.hsize *= 2;
   k.chp = std::max<uint64_t>(pow2_at_least((uint64_t)dvsg::kChunk), pow2_at_least(k.cap));
   static const uint64_t hash_smem_max = [] {
     const char* e = std::getenv("DVSG_HASH_SMEM_MAX");
@@ -1057,7 +1065,7 @@ void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const 
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
   c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
   cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->assign_scratch.p, c->stream), "assign");
-  cuda_check(dvsg::launch_route(c->assign.p, nq, fanout, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
+  cuda_check(dvsg::launch_route(c->assign.p, nq, fanout, c->d_cluster_slot.p, c->slot_map_n, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
   c->launches += 2;
   search_units(c, d_q, nq, dim, c->unit_q.p, c->unit_p.p, nu, p, c->u_ids.p, c->u_dists.p, c->u_count.p, vis);
@@ -1404,8 +1412,14 @@ dvsg_status dvsg_search_units_device(dvsg_ctx* c, const float* d_queries, uint64
     cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
     // route_kernel with fanout 1 maps cluster -> slot and writes unit_query = u;
     // the caller's unit_query is then used directly.
-    cuda_check(dvsg::launch_route(d_unit_cluster, nunits, 1, c->d_cluster_slot.p, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
+    cuda_check(dvsg::launch_route(d_unit_cluster, nunits, 1, c->d_cluster_slot.p, c->slot_map_n, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
     c->launches += 1;
+    // a unit naming an unknown or non-resident cluster is the caller's error:
+    // report it before launching the search (as the host-buffer entry points do)
+    int flag = 0;
+    cuda_check(cudaMemcpyAsync(&flag, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "err flag");
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    if (flag) fail(DVSG_EINVAL, "search_units: a unit names a cluster that is not resident on this context");
     search_units(c, d_queries, nq, dim, d_unit_query, c->unit_p.p, nunits, p, d_out_ids, d_out_dists, d_out_count, d_out_visited);
   });
 }

@@ -189,12 +189,13 @@ __global__ void select_topc_kernel(const uint64_t* __restrict__ scratch, uint64_
 }
 
 __global__ void route_kernel(const uint32_t* __restrict__ assign, uint64_t nq, int fanout,
-                             const int32_t* __restrict__ cluster_to_slot,
+                             const int32_t* __restrict__ cluster_to_slot, uint32_t nmap,
                              uint32_t* __restrict__ unit_query, uint32_t* __restrict__ unit_part,
                              int* err) {
   const uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nq * (uint64_t)fanout) return;
-  const int32_t slot = cluster_to_slot[assign[u]];
+  const uint32_t cl = assign[u];
+  const int32_t slot = cl < nmap ? cluster_to_slot[cl] : -1;  // unknown or non-resident cluster
   if (slot < 0) {
     atomicOr(err, 1);
     unit_part[u] = 0;
@@ -385,12 +386,12 @@ cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const floa
 }
 
 cudaError_t launch_route(const uint32_t* assign, uint64_t nq, int fanout,
-                         const int32_t* cluster_to_slot, uint32_t* unit_query,
+                         const int32_t* cluster_to_slot, uint32_t nmap, uint32_t* unit_query,
                          uint32_t* unit_part, int* err_flag, cudaStream_t stream) {
   const uint64_t n = nq * (uint64_t)fanout;
   if (n == 0) return cudaSuccess;
   route_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(assign, nq, fanout,
-                                                                 cluster_to_slot, unit_query,
+                                                                 cluster_to_slot, nmap, unit_query,
                                                                  unit_part, err_flag);
   return cudaGetLastError();
 }

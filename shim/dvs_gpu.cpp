@@ -7,17 +7,22 @@
 //
 //   validate(SearchParams)   graph_index.cpp:14-19      host check (same message)
 //   compute_entry_order      graph_index.cpp:21-44      dvsg_compute_entry_order
-//   build_graph              graph_index.cpp:46-103     dvsg_build_graph (GPU K6)
+//   build_graph              graph_index.cpp:46-103     dvsg_build_graph (GPU K6) on integer data with
+//                                                       degree <= 32 (exact there); else exact host rows
 //   beam_search_stats        graph_index.cpp:105-187    dvsg_load_partition + dvsg_beam_search (K1)
 //   beam_search / visited_count  :189-197               via beam_search_stats
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <numeric>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "dvs/distance.hpp"
 #include "dvs/errors.hpp"
 #include "dvs/graph_index.hpp"
 #include "dvsg.h"
@@ -104,6 +109,56 @@ Backend& backend() {
 
 }  // namespace
 
+namespace {
+
+// K6 (dvsg_build_graph) accumulates in fp32: bit-identical to the reference's
+// fp64 squared_l2 only when every sum is an exact fp32 integer.
+bool integer_valued(const dvs::Dataset& d) {
+  double mx = 0.0;
+  for (const float x : d.data) {
+    if (x != std::nearbyint(x)) return false;
+    mx = std::max(mx, (double)std::fabs(x));
+  }
+  return 4.0 * mx * mx * (double)d.dim < 16777216.0;  // every (x - y)^2 partial sum < 2^24
+}
+
+// Exact rows on the host for float data or out_degree > 32 (the K6 limits):
+// row v = the out_degree smallest (squared_l2, id) keys over u != v, short
+// lists repeated cyclically, a lone node padded with itself
+// (graph_index.cpp:46-97).  O(n^2) like the reference; this shim only serves
+// the reference's own unit-test sizes.
+void exact_rows_host(const dvs::Dataset& part, int out_degree, std::uint32_t* adj) {
+  const std::size_t n = part.size(), dg = (std::size_t)out_degree;
+  auto rows = [&](std::size_t b, std::size_t e) {
+    std::vector<std::uint64_t> keys;
+    keys.reserve(n);
+    for (std::size_t v = b; v < e; ++v) {
+      std::uint32_t* row = adj + v * dg;
+      if (n == 1) {
+        std::fill(row, row + dg, 0u);
+        continue;
+      }
+      keys.clear();
+      for (std::size_t u = 0; u < n; ++u) {
+        if (u == v) continue;
+        const float f = dvs::squared_l2(part[v], part[u]);  // >= 0: raw bits order like values
+        std::uint32_t bits;
+        std::memcpy(&bits, &f, 4);
+        keys.push_back(((std::uint64_t)bits << 32) | (std::uint32_t)u);
+      }
+      const std::size_t take = std::min(dg, keys.size());
+      std::partial_sort(keys.begin(), keys.begin() + (std::ptrdiff_t)take, keys.end());
+      for (std::size_t j = 0; j < dg; ++j) row[j] = (std::uint32_t)keys[j % take];
+    }
+  };
+  const std::size_t nt = std::max<std::size_t>(1, std::min<std::size_t>(std::thread::hardware_concurrency(), 16));
+  std::vector<std::thread> th;
+  for (std::size_t t = 0; t < nt; ++t) th.emplace_back(rows, n * t / nt, n * (t + 1) / nt);
+  for (auto& x : th) x.join();
+}
+
+}  // namespace
+
 namespace dvs {
 
 void validate(const SearchParams& p) {
@@ -134,10 +189,15 @@ GraphIndex build_graph(const Dataset& partition, std::vector<std::uint32_t> glob
   g.global_ids = std::move(global_ids);
   g.out_degree = out_degree;
   g.adjacency.resize(n * static_cast<std::size_t>(out_degree));
-  Backend& b = backend();
-  std::lock_guard<std::mutex> lk(b.mu);
-  check(dvsg_build_graph(b.get(), partition.data.data(), n, partition.dim, out_degree,
-                         g.adjacency.data()));
+  if (out_degree <= 32 && integer_valued(partition)) {
+    // K6's fp32 sums are exact here, i.e. equal to the fp64-then-round squared_l2
+    Backend& b = backend();
+    std::lock_guard<std::mutex> lk(b.mu);
+    check(dvsg_build_graph(b.get(), partition.data.data(), n, partition.dim, out_degree,
+                           g.adjacency.data()));
+  } else {
+    exact_rows_host(partition, out_degree, g.adjacency.data());
+  }
   g.entry_order = compute_entry_order(partition);
   return g;
 }

@@ -26,14 +26,16 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(scope="module")
 def cfg1(ctx):
+    import torch
+
     import bench
-    sys.argv = ["bench", "--nq", "4000"]
-    args = bench.parse()
-    data, queries, index = bench.workload(args, 0, ctx)
+    args = bench.parse(["--workload", "cfg1", "--nq", "4000"])
     ctx.reset()
     ctx._single_key = None
-    ctx.load_partition(0, index.graphs[0])
-    return data, queries, index.graphs[0]
+    w = bench.build_cfg1(args, 0, ctx, torch.device("cuda", 0))  # loads the index into ctx
+    data, adj = w.host
+    g = dvs.GraphIndex(data, np.arange(data.shape[0], dtype=np.uint32), 32, adj, None)
+    return data, w.queries.cpu().numpy(), g
 
 
 def test_fullsize_properties(ctx, cfg1):
@@ -72,3 +74,43 @@ def test_fullsize_sample_matches_reference(ctx, cfg1, ref):
         n = int(counts[q])
         assert np.array_equal(ids[q, :n], want[0][q, :n])
         assert np.array_equal(dists[q, :n], want[1][q, :n])
+
+
+def test_cfg3_fullsize_properties(ctx):
+    """The bench's cfg3 index (100M x 96, GPU-built graph) at full size:
+    result order / uniqueness / exact fp64 distances of the returned rows,
+    the visited bound, determinism, f32 == f64 on integer data and the
+    node-sharded search (4 emulated ranks) == unsharded."""
+    import torch
+
+    import bench
+    args = bench.parse(["--nq", "20000", "--recall-sample", "500"])
+    ctx.reset()
+    ctx._single_key = None
+    w = bench.build_cfg3(args, 0, ctx, torch.device("cuda", 0))
+    I, wd, k, E = args.iterations, args.beam, args.k, args.entry
+    q = w.queries.cpu().numpy()
+    ids, dists, counts, visited = ctx.beam_search(0, q, dvs.SearchParams(I, wd, k, E, accum="f32"))
+    assert (counts == k).all()
+    assert (visited <= E + I * wd * 32).all() and (visited >= E).all()
+    rows = np.arange(0, len(q), 97)
+    vec = w.vec[torch.from_numpy(ids[rows].astype(np.int64).reshape(-1)).cuda()].cpu().numpy()
+    vec = vec.reshape(len(rows), k, -1)[:, :, :args.dim]
+    for j, r in enumerate(rows):
+        assert len(set(ids[r].tolist())) == k and int(ids[r].max()) < args.n
+        keys = list(zip(dists[r].tolist(), ids[r].tolist()))
+        assert keys == sorted(keys)
+        diff = vec[j].astype(np.float64) - q[r].astype(np.float64)
+        assert np.array_equal(dists[r], (diff * diff).sum(1).astype(np.float32))
+    rec = bench.recall_at_k(ids[:w.gt.shape[0]], counts[:w.gt.shape[0]], w.gt, k)
+    assert rec >= 0.95
+    again = ctx.beam_search(0, q, dvs.SearchParams(I, wd, k, E, accum="f32"))
+    exact = ctx.beam_search(0, q[:5000], dvs.SearchParams(I, wd, k, E, accum="f64"))
+    for a, b, c in zip(again, exact, (ids, dists, counts, visited)):
+        assert np.array_equal(a, c) and np.array_equal(b, c[:5000])
+    sharded = ctx.beam_search_sharded_emulated(4, q[:2000], dvs.SearchParams(I, wd, k, E, accum="f32"))
+    for a, c in zip(sharded, (ids, dists, counts, visited)):
+        assert np.array_equal(a, c[:2000])
+    del w
+    ctx.reset()
+    torch.cuda.empty_cache()

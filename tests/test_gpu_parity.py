@@ -1,7 +1,9 @@
 """GPU parity: the sm_100a path through the C-ABI against the oracle and the
 reference's golden fixtures.  Bar: integer/index outputs bit-exact (ids,
-counts, visited); distances bit-exact in f64 mode and on integer data,
-<= 1e-4 relative in f32 mode on float data (north_star tolerance)."""
+counts, visited); distances bit-exact in f64 mode and on integer data.  The
+f32 mode is exact on integer data and is upgraded to a parity mode (f64, or
+f32c for inner product / wide rows) on float data; at scale the float-data
+bar is north_star's (>= 99.9% identical id lists, 1e-4 relative)."""
 import os
 
 import numpy as np
@@ -49,13 +51,9 @@ def test_search_matches_reference_golden(ctx, golden, fixture, accum):
         p = dvs.SearchParams(int(I), int(w), int(k), int(E), accum=accum)
         got = _search(ctx, v, adj, q, p, gids)
         want = (g[f"ids{i}"], g[f"dists{i}"], g[f"counts{i}"], g[f"visited{i}"])
-        exact = accum == "f64" or fixture.startswith("g2")  # integer data: f32 is exact
-        if exact:
-            _assert_same(got, want, True, (fixture, i))
-        else:  # f32 on float data: >= 99.9% identical id lists, dists 1e-4
-            same = sum(np.array_equal(got[0][j, :got[2][j]], want[0][j, :want[2][j]])
-                       for j in range(len(q)))
-            assert same >= 0.99 * len(q)
+        # f64 always; f32 is exact on integer data (g2) and upgraded to a parity
+        # mode on float data (g1), so every case is bit-exact
+        _assert_same(got, want, True, (fixture, i, accum))
 
 
 def test_entry_order_on_upload_matches_reference(ctx, golden):
@@ -525,10 +523,43 @@ def test_cfg4_shape_ip768_k100_beam256(ctx, oracle):
     want = oracle.beam_search(v, gids, adj, eo, q, 6, 256, 100, 256, metric=1)
     got = _search(ctx, v, adj, q, dvs.SearchParams(6, 256, 100, 256, metric="ip", accum="f64"))
     _assert_same(got, want, True, "cfg4-shape f64")
+    # f32 requested on float data runs in the compensated mode (f32c): the
+    # north_star bar is >= 99.9% identical id lists, i.e. all 24 here
     got32 = _search(ctx, v, adj, q, dvs.SearchParams(6, 256, 100, 256, metric="ip", accum="f32"))
     same = sum(np.array_equal(got32[0][j, :got32[2][j]], want[0][j, :want[2][j]]) for j in range(len(q)))
-    assert same >= 0.9 * len(q)
+    assert same >= int(np.ceil(0.999 * len(q)))
     np.testing.assert_allclose(got32[1][:, :10], want[1][:, :10], rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("metric", ["l2", "ip"])
+def test_f64_float_data_10k_queries_768d(ctx, oracle, metric):
+    """The f64 mode on float data at scale: 10k queries at 768-d against the
+    oracle's sequential fp64 (distance.cpp:19-27 order).  The kernel sums lane
+    partials through a tree, so bit identity is observed, not guaranteed; the
+    bar is north_star's (>= 99.9% identical id lists, 1e-4 relative) and the
+    test reports how many lists / distances actually differ."""
+    n, dim, nq = 20000, 768, 10000
+    rng = np.random.default_rng(8)
+    basis = rng.normal(size=(32, dim)).astype(np.float32)
+    v = rng.normal(size=(n, 32)).astype(np.float32) @ basis + 0.05 * rng.normal(size=(n, dim)).astype(np.float32)
+    q = rng.normal(size=(nq, 32)).astype(np.float32) @ basis + 0.05 * rng.normal(size=(nq, dim)).astype(np.float32)
+    if metric == "ip":
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        q /= np.linalg.norm(q, axis=1, keepdims=True)
+    adj = ctx.build_graph(v, 32)  # any graph will do: both sides search the same one
+    eo = oracle.compute_entry_order(v)
+    gids = np.arange(n, dtype=np.uint32)
+    want = oracle.beam_search(v, gids, adj, eo, q, 6, 32, 10, 32, metric=1 if metric == "ip" else 0,
+                              nthreads=16)
+    got = _search(ctx, v, adj, q, dvs.SearchParams(6, 32, 10, 32, metric=metric, accum="f64"), eo=eo)
+    same = sum(np.array_equal(got[0][j, :got[2][j]], want[0][j, :want[2][j]]) for j in range(nq))
+    dist_same = int(np.sum(np.all(got[1] == want[1], axis=1)))
+    print(f"f64 {metric} 768-d: {same}/{nq} id lists and {dist_same}/{nq} distance rows bit-identical")
+    assert same >= int(np.ceil(0.999 * nq))
+    np.testing.assert_allclose(got[1], want[1], rtol=1e-4, atol=1e-6)
+    vis_same = int(np.sum(got[3] == want[3]))
+    print(f"  visited counters equal on {vis_same}/{nq} queries")
+    assert vis_same >= int(np.ceil(0.999 * nq))
 
 
 def test_cfg3_shape_d96_beam_sweep(ctx, oracle):
