@@ -66,6 +66,11 @@ WORKLOADS = {
                       "latent), degree-32 graph (GPU-built: cluster-restricted kNN + CAGRA-style rank "
                       "pruning / reverse edges) in 1 partition, 1M-query batch per GPU, top-10, beam 16, "
                       "I=24, entry 16"),
+    "cfg4": dict(n=10_000_000, dim=768, nq=100_000, iterations=16, beam=256, entry=256, k=100, degree=32,
+                 graph="ivf", metric="ip", rank_latent=32, accum="f32c",
+                 desc="BASELINE configs[3]: text-embedding-like synthetic 10M x 768 (float, rank-32 latent, "
+                      "L2-normalised), inner product, GPU-built degree-32 graph in 1 partition, 100k-query batch "
+                      "per GPU, top-100, beam 256, I=16, entry 256, compensated-f32 distances (f32c)"),
     "cfg1": dict(n=1_000_000, dim=128, nq=100_000, iterations=6, beam=64, entry=64, k=10, degree=32,
                  graph="exact",
                  desc="BASELINE configs[1] at N=1: SIFT-like synthetic 1M x 128 (integer-valued f32, "
@@ -84,13 +89,13 @@ def parse(argv=None):
     ap.add_argument("--n", "--rows", dest="n", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--dim", type=int, default=None)
-    ap.add_argument("--rank-latent", type=int, default=16)
+    ap.add_argument("--rank-latent", type=int, default=None)
     ap.add_argument("--degree", type=int, default=None)
     ap.add_argument("--iterations", type=int, default=None)
     ap.add_argument("--beam", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--entry", type=int, default=None)
-    ap.add_argument("--accum", choices=["f32", "f64", "f32c"], default="f32")
+    ap.add_argument("--accum", choices=["f32", "f64", "f32c"], default=None)
     ap.add_argument("--probe", type=int, default=8, help="cfg3 graph build: clusters probed per row")
     ap.add_argument("--cluster-size", type=int, default=1024, help="cfg3 graph build: rows per cluster")
     ap.add_argument("--keep", type=int, default=12,
@@ -115,12 +120,13 @@ def parse(argv=None):
                          "round trips (shard_kernel.cu), or the bulk protocol over host-driven NCCL "
                          "send/recv (the measured baseline)")
     a = ap.parse_args(argv)
-    for key, v in WORKLOADS[a.workload].items():
+    wl = dict(dict(rank_latent=16, accum="f32", metric="l2"), **WORKLOADS[a.workload])
+    for key, v in wl.items():
         if key in ("graph", "desc"):
             continue
-        if getattr(a, key) is None:
+        if getattr(a, key, None) is None:
             setattr(a, key, v)
-    a.graph = WORKLOADS[a.workload]["graph"]
+    a.graph = wl["graph"]
     return a
 
 
@@ -232,7 +238,10 @@ def build_cfg3(args, rank, ctx, dev, gt_rows=None):
     from paper_2512_02278_b200 import ivf
     t0 = time.time()
     dpad = (args.dim + 3) // 4 * 4
-    x = ivf.sift_like_device(args.n, args.dim, args.rank_latent, seed=1, device=dev, dpad=dpad)
+    if args.metric == "ip":
+        x = ivf.embedding_like_device(args.n, args.dim, rank=args.rank_latent, seed=3, device=dev)
+    else:
+        x = ivf.sift_like_device(args.n, args.dim, args.rank_latent, seed=1, device=dev, dpad=dpad)
     info = ivf.build_graph_ivf(ctx, x, degree=args.degree, cluster_size=args.cluster_size, probe=args.probe,
                                dim=args.dim, optimize=True, keep=args.keep, log=log)
     del x
@@ -246,10 +255,15 @@ def build_cfg3(args, rank, ctx, dev, gt_rows=None):
         acc += vec[b:b + (1 << 24)].double().sum(0)
     cent = (acc / n).float()[:args.dim].cpu().numpy()[None, :]
     ctx.set_centroids(cent, np.zeros(1, np.uint32), 1)
-    q = ivf.sift_like_queries_device(args.nq, args.dim, args.rank_latent, data_seed=1, seed=2 + rank,
-                                     device=dev)
     s = min(args.recall_sample, args.nq) if gt_rows is None else gt_rows
-    gt, _ = ivf.brute_force_topk(ctx, vec, ivf.row_norms(ctx, vec), q[:s].contiguous(), args.k)
+    if args.metric == "ip":
+        q = ivf.embedding_like_device(args.nq, args.dim, rank=args.rank_latent, seed=4 + rank, basis_seed=3,
+                                      device=dev)
+        gt = ivf.topk_ip_device(vec, q[:s].contiguous(), args.k)
+    else:
+        q = ivf.sift_like_queries_device(args.nq, args.dim, args.rank_latent, data_seed=1, seed=2 + rank,
+                                         device=dev)
+        gt, _ = ivf.brute_force_topk(ctx, vec, ivf.row_norms(ctx, vec), q[:s].contiguous(), args.k)
     w = Workload()
     w.queries = q
     w.gt = gt.cpu().numpy()
@@ -258,7 +272,7 @@ def build_cfg3(args, rank, ctx, dev, gt_rows=None):
     w.adj = ivf.device_view(pa, (n, args.degree), torch.int32, dev)
     w.info = {k: v for k, v in info.items()}
     w.info["setup_s"] = time.time() - t0
-    log(f"[bench] cfg3 workload ready in {w.info['setup_s']:.1f}s")
+    log(f"[bench] {args.workload} workload ready in {w.info['setup_s']:.1f}s")
     return w
 
 
@@ -299,7 +313,7 @@ def build_cfg1(args, rank, ctx, dev, gt_rows=None):
 
 
 def build_workload(args, rank, ctx, dev, gt_rows=None):
-    return (build_cfg3 if args.workload == "cfg3" else build_cfg1)(args, rank, ctx, dev, gt_rows)
+    return (build_cfg1 if args.workload == "cfg1" else build_cfg3)(args, rank, ctx, dev, gt_rows)
 
 
 def host_index(w):
@@ -362,12 +376,17 @@ def reference_setup(args):
     ctx.close()
 
 
-def ref_index(vec, adj, centroid, degree):
+def ref_index(vec, adj, centroid, degree, metric="l2"):
     """The reference's own BuiltIndex over these arrays (oracle/_ref: the
-    unmodified reference sources; compute_entry_order is the reference's)."""
+    unmodified reference sources; compute_entry_order is the reference's).
+    Inner product has no reference implementation (SPEC.md: L2 only): the
+    oracle's restatement (dist = -dot, same tie rules) stands in ("port")."""
     from oracle.oracle import Oracle, Ref, have_ref
     n = vec.shape[0]
     gids = np.arange(n, dtype=np.uint32)
+    if metric == "ip":
+        o = Oracle()
+        return "port", (o, (vec, gids, adj, o.compute_entry_order(vec)))
     if have_ref():
         return "reference", Ref().index_from_arrays(centroid, np.zeros(1, np.uint32), 1, degree,
                                                     [(vec, adj, gids)])
@@ -381,6 +400,13 @@ def ref_runner(kind, idx, args, nthreads):
         def run(qs):
             return idx.run_pipeline(qs, args.iterations, args.beam, args.k, args.entry, 1, 1,
                                     nthreads=nthreads, with_vectors=True)
+    elif args.metric == "ip":
+        o, (vec, gids, adj, eo) = idx
+
+        def run(qs):  # C = 1: run_pipeline is one beam search per query (simulator.cpp:317-324)
+            ids, dists, counts, vis = o.beam_search(vec, gids, adj, eo, qs, args.iterations, args.beam, args.k,
+                                                    args.entry, metric=1, nthreads=nthreads)
+            return ids, dists, counts, None, int(vis.sum())
     else:
         o, bi = idx
 
@@ -411,7 +437,8 @@ def run_reference_impl(args, world, rank):
                "--workload", args.workload, "--n", str(args.n), "--nq", str(args.nq), "--dim", str(args.dim),
                "--rank-latent", str(args.rank_latent), "--degree", str(args.degree),
                "--probe", str(args.probe), "--cluster-size", str(args.cluster_size), "--keep", str(args.keep),
-               "--k", str(args.k), "--recall-sample", str(args.recall_sample), "--cache", args.cache]
+               "--k", str(args.k), "--recall-sample", str(args.recall_sample), "--cache", args.cache,
+               "--iterations", str(args.iterations), "--beam", str(args.beam), "--entry", str(args.entry)]
         env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
         subprocess.run(cmd, check=True, env=env, stdout=sys.stderr)
         vec = np.load(os.path.join(out, "vectors.npy"), mmap_mode="r")
@@ -420,7 +447,9 @@ def run_reference_impl(args, world, rank):
         queries = np.load(os.path.join(out, "queries.npy"))
         gt = np.load(os.path.join(out, "gt.npy"))
         meta = json.load(open(os.path.join(out, "meta.json")))
-        kind, idx = ref_index(vec, adj, centroid, args.degree)
+        kind, idx = ref_index(np.ascontiguousarray(vec) if args.metric == "ip" else vec,
+                              np.ascontiguousarray(adj) if args.metric == "ip" else adj, centroid, args.degree,
+                              args.metric)
         del vec, adj
     finally:
         shutil.rmtree(out, ignore_errors=True)
@@ -441,8 +470,10 @@ def run_reference_impl(args, world, rank):
     total = sum(times)
     qps = n * args.steps / total
     s = min(gt.shape[0], n)
-    rec = recall_at_k(res[0][:s], res[2][:s], gt[:s], args.k)
+    rec = recall_at_k(res[0][:s, :10], np.minimum(res[2][:s], 10), gt[:s, :10], 10)
     cfg = workload_config(args, world, rec)
+    if args.k != 10:
+        cfg[f"recall_at_{args.k}"] = round(recall_at_k(res[0][:s], res[2][:s], gt[:s], args.k), 4)
     cfg["graph"] = dict(meta["graph"], adjacency_sha256=meta["adjacency_sha256"])
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
@@ -548,9 +579,12 @@ def e2e_pinned(args, torch, dvs, ctx, w, p, ids_h, cnt_h, flush, dist, world, ra
 
     hq = pin((nq, dim), torch.float32)
     hq[:] = w.queries[:, :dim].cpu().numpy()
+    wv = args.workload != "cfg4"  # hit vectors (off at cfg4: 30.7 GB per step)
     out = {"ids": pin((nq, k), torch.int32).view(np.uint32), "dists": pin((nq, k), torch.float32),
-           "counts": pin((nq,), torch.int32).view(np.uint32), "vectors": pin((nq, k, dim), torch.float32)}
-    ctx.run_pipeline(hq, p, 1, 1, 0, True, out)  # warm
+           "counts": pin((nq,), torch.int32).view(np.uint32)}
+    if wv:
+        out["vectors"] = pin((nq, k, dim), torch.float32)
+    ctx.run_pipeline(hq, p, 1, 1, 0, wv, out)  # warm
     stream = torch.cuda.ExternalStream(ctx.stream, device=flush.device)
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -561,7 +595,7 @@ def e2e_pinned(args, torch, dvs, ctx, w, p, ids_h, cnt_h, flush, dist, world, ra
         flush.fill_(float(i))
         torch.cuda.synchronize()
         ev0[i].record(stream)
-        ctx.run_pipeline(hq, p, 1, 1, 0, True, out)
+        ctx.run_pipeline(hq, p, 1, 1, 0, wv, out)
         ev1[i].record(stream)
     torch.cuda.synchronize()
     e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))], dtype=torch.float64,
@@ -571,20 +605,19 @@ def e2e_pinned(args, torch, dvs, ctx, w, p, ids_h, cnt_h, flush, dist, world, ra
     assert np.array_equal(out["ids"], ids_h) and np.array_equal(out["counts"], cnt_h), \
         "host-buffer and device-pointer paths disagree"
     h2d = hq.nbytes
-    d2h = out["ids"].nbytes + out["dists"].nbytes + out["counts"].nbytes + out["vectors"].nbytes + 4 + 8
+    d2h = sum(v.nbytes for v in out.values()) + 4 + 8
     e2e = {"value": nq * world * args.steps / (float(e_ms[0]) / 1e3), "unit": "queries/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": float(e_ms[0]) / args.steps, "host_buffers": "pinned",
            "timeline": timeline_summary(dvs, ctx.last_pipeline_timeline(rank), args)}
     # the drop-in caller of INTEGRATION.md passes ordinary (pageable) memory
     qp = np.array(hq)
-    outp = {"ids": np.zeros((nq, k), np.uint32), "dists": np.zeros((nq, k), np.float32),
-            "counts": np.zeros(nq, np.uint32), "vectors": np.zeros((nq, k, dim), np.float32)}
-    ctx.run_pipeline(qp, p, 1, 1, 0, True, outp)
+    outp = {kk: np.zeros_like(v) for kk, v in out.items()}
+    ctx.run_pipeline(qp, p, 1, 1, 0, wv, outp)
     reps = max(1, min(args.steps, 3))
     t0 = time.perf_counter()
     for _ in range(reps):
-        ctx.run_pipeline(qp, p, 1, 1, 0, True, outp)
+        ctx.run_pipeline(qp, p, 1, 1, 0, wv, outp)
     dt = (time.perf_counter() - t0) / reps
     e2e["pageable"] = {"value": nq / dt, "unit": "queries/s", "ms_per_step": 1e3 * dt, "steps": reps,
                        "timing": "host wall clock around dvsg_run_pipeline (synchronous call)",
@@ -602,7 +635,7 @@ def accum_modes(args, torch, dvs, ctx, w, ids_h, cnt_h, dev):
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     out = {}
     for mode in ("f64", "f32c"):
-        p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=mode)
+        p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, metric=args.metric, accum=mode)
         torch.cuda.synchronize()
 
         def run():
@@ -627,7 +660,7 @@ def cpu_baseline(args, w, ids_h, cnt_h, dists_h):
     nthreads = os.cpu_count() or 1
     t0 = time.time()
     vec, adj = host_index(w)
-    kind, idx = ref_index(vec, adj, w.centroid, args.degree)
+    kind, idx = ref_index(vec, adj, w.centroid, args.degree, args.metric)
     if w.graph_sha256 is None:
         w.graph_sha256 = sha256_bytes(adj)
     del vec, adj
@@ -658,7 +691,7 @@ def sharded_measure(args, torch, dvs, dist, ctx, w, rank, world, local, flush, i
     if args.exchange == "nccl":
         connect_nccl(ctx, rank)
     nq, dim = args.nq, args.dim
-    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, metric=args.metric, accum=args.accum)
     b = Bufs(torch, nq, args.k, dim, dev, vectors=False)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
 
@@ -780,16 +813,17 @@ def main():
 
     ctx = dvs.Context(local)
     w = build_workload(args, rank, ctx, dev)
-    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+    p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, metric=args.metric, accum=args.accum)
     nq, dim, k = args.nq, args.dim, args.k
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    b = Bufs(torch, nq, k, dim, dev)
+    with_vectors = args.workload != "cfg4"  # 100k x 100 x 768 hit vectors would be 30.7 GB per step
+    b = Bufs(torch, nq, k, dim, dev, vectors=with_vectors)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     torch.cuda.synchronize()
 
     def step():
         ctx.run_pipeline_device(w.queries.data_ptr(), nq, dim, p, 1, b.ids.data_ptr(), b.dists.data_ptr(),
-                                b.counts.data_ptr(), b.vecs.data_ptr())
+                                b.counts.data_ptr(), b.vecs.data_ptr() if with_vectors else 0)
 
     # ---- the replica / single-GPU run_pipeline (headline at N = 1) ----------------
     ctx.set_timing(True)
@@ -800,7 +834,8 @@ def main():
     cnt_h = b.counts.cpu().numpy().view(np.uint32)
     dists_h = b.dists.cpu().numpy()
     s = w.gt.shape[0]
-    rec = recall_at_k(ids_h[:s], cnt_h[:s], w.gt, k)
+    rec = recall_at_k(ids_h[:s, :10], np.minimum(cnt_h[:s], 10), w.gt[:, :10], 10)  # the metric's recall@10
+    rec_k = recall_at_k(ids_h[:s], cnt_h[:s], w.gt, k)
     replica = {"value": nq * world * args.steps / (total_ms / 1e3), "unit": "queries/s",
                "ms_per_step": total_ms / args.steps, "recall_at_10": round(rec, 4)}
 
@@ -816,7 +851,7 @@ def main():
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "queries/s", "cores": 0, "kind": "unavailable",
                    "sample": f"failed: {type(ex).__name__}: {ex}"}
-    elif rank == 0 and args.workload == "cfg3" and w.graph_sha256 is None:
+    elif rank == 0 and args.workload != "cfg1" and w.graph_sha256 is None:
         w.graph_sha256 = sha256_bytes(w.adj.cpu().numpy())
 
     # ---- N > 1: the node-sharded north-star layout is the headline ------------------
@@ -855,7 +890,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": eff_accum, "data": "synthetic",
-        "config": workload_config(args, world, rec, w, sharded=bool(headline)),
+        "config": dict(workload_config(args, world, rec, w, sharded=bool(headline)),
+                       **({f"recall_at_{k}": round(rec_k, 4)} if k != 10 else {})),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": tsrc,
                      "peak_kind": peak_kind, "kernel": "dvsg::search_kernel (K1)",

@@ -389,3 +389,47 @@ def sift_like_queries_device(nq: int, dim: int, rank: int = 16, data_seed: int =
     out = torch.zeros((nq, dpad), dtype=torch.float32, device=device)
     out[:, :dim] = torch.clamp(torch.round(torch.addmm(eps, z, a, beta=0.1) * scale + 128.0), 0.0, 255.0)
     return out
+
+
+def embedding_like_device(n: int, dim: int = 768, rank: int = 32, seed: int = 3, noise: float = 0.05,
+                          device="cuda:0", chunk: int = 1 << 21, out=None, basis_seed: Optional[int] = None):
+    """Text-embedding-like float data for BASELINE configs[3]:
+    x = z B + noise * eps with z ~ N(0, I_rank), B ~ N(0, 1) (rank x dim), rows
+    L2-normalised.  Float-valued: the search runs in a parity mode (f32c/f64).
+    `basis_seed` (default `seed`) fixes B, so queries can share the data's B."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed if basis_seed is None else basis_seed))
+    b = torch.randn((rank, dim), generator=g, device=device, dtype=torch.float32)
+    if basis_seed is not None:
+        g.manual_seed(int(seed))
+    if out is None:
+        out = torch.empty((n, dim), dtype=torch.float32, device=device)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        z = torch.randn((e - s, rank), generator=g, device=device, dtype=torch.float32)
+        eps = torch.randn((e - s, dim), generator=g, device=device, dtype=torch.float32)
+        xb = torch.addmm(eps, z, b, beta=noise, alpha=1.0)
+        out[s:e] = xb / torch.linalg.vector_norm(xb, dim=1, keepdim=True)
+    return out
+
+
+def topk_ip_device(db, queries, k: int, chunk: int = 1 << 21):
+    """Exact-order top-k by (f32(-dot), id) over all rows -- the inner-product
+    restatement of brute_force_topk (topk.cpp:12-30) for ground truth at
+    k > 32.  dot in fp64 per chunk (torch), then rounded to f32 like the
+    search's distances.  -> int64 ids (nq x k)."""
+    import torch
+    n = db.shape[0]
+    best = None
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        d = -(queries.double() @ db[s:e].double().T)
+        key = (d.float().contiguous().view(torch.int32).to(torch.int64))
+        # order-preserving map of the f32 bit pattern, then id as the tie-break
+        key = torch.where(key < 0, ~key & 0xFFFFFFFF, key | 0x80000000)
+        key = (key << 32) | torch.arange(s, e, device=db.device, dtype=torch.int64)[None, :]
+        key = key ^ (1 << 63)  # int64 compare on the unsigned key
+        cand = torch.topk(key, min(k, e - s), dim=1, largest=False).values
+        best = cand if best is None else torch.topk(torch.cat([best, cand], 1), k, dim=1, largest=False).values
+    return (best ^ (1 << 63)) & 0xFFFFFFFF
