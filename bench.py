@@ -67,10 +67,10 @@ WORKLOADS = {
                       "pruning / reverse edges) in 1 partition, 1M-query batch per GPU, top-10, beam 16, "
                       "I=24, entry 16"),
     "cfg4": dict(n=10_000_000, dim=768, nq=100_000, iterations=16, beam=256, entry=256, k=100, degree=32,
-                 graph="ivf", metric="ip", rank_latent=32, accum="f32c",
+                 graph="ivf", metric="ip", rank_latent=32, accum="f64",
                  desc="BASELINE configs[3]: text-embedding-like synthetic 10M x 768 (float, rank-32 latent, "
                       "L2-normalised), inner product, GPU-built degree-32 graph in 1 partition, 100k-query batch "
-                      "per GPU, top-100, beam 256, I=16, entry 256, compensated-f32 distances (f32c)"),
+                      "per GPU, top-100, beam 256, I=16, entry 256, f64 parity-mode distances"),
     "cfg1": dict(n=1_000_000, dim=128, nq=100_000, iterations=6, beam=64, entry=64, k=10, degree=32,
                  graph="exact",
                  desc="BASELINE configs[1] at N=1: SIFT-like synthetic 1M x 128 (integer-valued f32, "

@@ -414,13 +414,14 @@ def embedding_like_device(n: int, dim: int = 768, rank: int = 32, seed: int = 3,
     return out
 
 
-def topk_ip_device(db, queries, k: int, chunk: int = 1 << 21):
+def topk_ip_device(db, queries, k: int, chunk: int = 0):
     """Exact-order top-k by (f32(-dot), id) over all rows -- the inner-product
     restatement of brute_force_topk (topk.cpp:12-30) for ground truth at
     k > 32.  dot in fp64 per chunk (torch), then rounded to f32 like the
     search's distances.  -> int64 ids (nq x k)."""
     import torch
     n = db.shape[0]
+    chunk = chunk or max(4096, (1 << 27) // max(1, queries.shape[0]))  # ~1 GB per int64 temporary
     best = None
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
