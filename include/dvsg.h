@@ -241,6 +241,25 @@ dvsg_status dvsg_run_pipeline_device(dvsg_ctx *ctx, const float *d_queries, uint
 dvsg_status dvsg_build_graph(dvsg_ctx *ctx, const float *vectors, uint64_t n, int dim,
                              int out_degree, uint32_t *adjacency_out);
 
+/* ---- partitioning (kmeans_train kmeans.cpp:189-241, partition_database
+ *      :282-300; build_index index.cpp:43-72 composes them) ---------------- */
+
+/* kmeans_train on the GPU with the reference's control flow and rounding:
+ * k-means++ seeding from std::mt19937_64(seed), Lloyd iterations with
+ * repair_empty_clusters and the fixed-point test, the final non-empty check.
+ * db: n x dim host rows; centroids_out: clusters x dim; iterations_out and
+ * wcss_out (max_iters doubles) may be NULL (KmeansStats, kmeans.hpp:27-30).
+ * Bit-identical to the reference on integer-valued data (kmeans++ prefix sums
+ * exact); errors as the reference (DVSG_EINVAL). */
+dvsg_status dvsg_kmeans_train(dvsg_ctx *ctx, const float *db, uint64_t n, int dim, int clusters,
+                              int max_iters, uint64_t seed, float *centroids_out,
+                              int *iterations_out, double *wcss_out);
+/* partition_database: the nearest centroid of every row (expanded_dist,
+ * ties to the lower id) -> labels_out[n]; the reference's per-cluster id
+ * lists are the rows of each label in row order. */
+dvsg_status dvsg_partition_database(dvsg_ctx *ctx, const float *db, uint64_t n, int dim,
+                                    const float *centroids, int clusters, uint32_t *labels_out);
+
 /* ---- ground truth (brute_force_topk, topk.cpp:12-30) ---------------------
  * Exact top-k by (dist, id) of nq queries over the n x dim database (host
  * buffers), k <= 32; fp32 distances over (x - y)^2, exact for integer-valued

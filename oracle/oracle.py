@@ -346,6 +346,28 @@ class Ref:
                                                  max_iters, seed, _p(out)))
         return out
 
+    def kmeans_train_stats(self, db, clusters, max_iters, seed):
+        """-> (centroids, iterations, wcss per iteration) -- KmeansStats (kmeans.hpp:27-30)."""
+        db = np.ascontiguousarray(db, np.float32)
+        out = np.zeros((clusters, db.shape[1]), np.float32)
+        it = c_int(0)
+        wcss = np.zeros(max(max_iters, 1), np.float64)
+        self.lib.dvsref_kmeans_train_stats.argtypes = [c_void_p, c_uint64, c_int, c_int, c_int, c_uint64,
+                                                        c_void_p, POINTER(c_int), c_void_p]
+        self._check(self.lib.dvsref_kmeans_train_stats(_p(db), db.shape[0], db.shape[1], clusters, max_iters,
+                                                       seed, _p(out), ctypes.byref(it), _p(wcss)))
+        return out, it.value, wcss[:it.value]
+
+    def partition_labels(self, db, cents):
+        """partition_database (kmeans.cpp:282-300) as a label per row."""
+        db = np.ascontiguousarray(db, np.float32)
+        cents = np.ascontiguousarray(cents, np.float32)
+        lab = np.zeros(db.shape[0], np.uint32)
+        self.lib.dvsref_partition_database.argtypes = [c_void_p, c_uint64, c_int, c_void_p, c_int, c_void_p]
+        self._check(self.lib.dvsref_partition_database(_p(db), db.shape[0], db.shape[1], _p(cents),
+                                                       cents.shape[0], _p(lab)))
+        return lab
+
     def build_index(self, db, clusters, out_degree, ranks, ranks_per_node, kmeans_iters, seed):
         db = np.ascontiguousarray(db, np.float32)
         h = self.lib.dvsref_build_index(_p(db), db.shape[0], db.shape[1], clusters, out_degree,

@@ -242,6 +242,29 @@ int dvsref_kmeans_train(const float* db, std::uint64_t n, int dim, int clusters,
   });
 }
 
+int dvsref_kmeans_train_stats(const float* db, std::uint64_t n, int dim, int clusters, int max_iters,
+                              std::uint64_t seed, float* out_centers, int* iterations, double* wcss) {
+  return guarded([&] {
+    dvs::KmeansStats st;
+    const auto c = dvs::kmeans_train(make_ds(db, n, dim), clusters, max_iters, seed, &st);
+    std::memcpy(out_centers, c.centers.data(), c.centers.size() * 4);
+    *iterations = st.iterations;
+    for (std::size_t i = 0; i < st.wcss.size(); ++i) wcss[i] = st.wcss[i];
+  });
+}
+
+int dvsref_partition_database(const float* db, std::uint64_t n, int dim, const float* cents, int clusters,
+                              std::uint32_t* labels) {
+  return guarded([&] {
+    dvs::Centroids ce;
+    ce.dim = dim;
+    ce.centers.assign(cents, cents + static_cast<std::size_t>(clusters) * dim);
+    const auto parts = dvs::partition_database(make_ds(db, n, dim), ce);
+    for (std::size_t c = 0; c < parts.size(); ++c)
+      for (const std::uint32_t id : parts[c]) labels[id] = static_cast<std::uint32_t>(c);
+  });
+}
+
 // build_index, index.cpp:43-72
 void* dvsref_build_index(const float* db, std::uint64_t n, int dim, int clusters, int out_degree,
                          int ranks, int ranks_per_node, int kmeans_iters, std::uint64_t seed) {

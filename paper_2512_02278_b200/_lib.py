@@ -105,6 +105,9 @@ _SIGS = {
                                             POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p)]),
     "dvsg_partition_commit_device": (c_int, [c_void_p, c_int]),
     "dvsg_index_integral": (c_int, [c_void_p, POINTER(c_int)]),
+    "dvsg_kmeans_train": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_int, c_uint64, c_void_p,
+                                  POINTER(c_int), c_void_p]),
+    "dvsg_partition_database": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_int, c_void_p]),
     "dvsg_optimize_graph_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int]),
     "dvsg_partition_view_device": (c_int, [c_void_p, c_uint32, POINTER(c_void_p), POINTER(c_void_p),
                                            POINTER(c_void_p), POINTER(c_void_p), POINTER(c_uint64)]),

@@ -41,7 +41,8 @@ __all__ = [
     "Context", "default_context", "beam_search_stats", "beam_search", "visited_count",
     "beam_search_batch", "compute_entry_order", "build_graph", "combine_results",
     "assign_top_c", "place_clusters", "route", "run_pipeline", "load_index", "save_index",
-    "check_timeline", "InvalidArgument", "FormatError", "InternalError",
+    "check_timeline", "InvalidArgument", "FormatError", "InternalError", "kmeans_train",
+    "partition_database", "build_index", "KmeansStats",
 ]
 
 
@@ -669,6 +670,62 @@ def assign_top_c(centroids, queries, c: int, ctx: Optional[Context] = None) -> n
     cx._single_key = None
     cx.set_centroids(cents, None, 1)
     return cx.assign_top_c(q, c)
+
+
+@dataclass
+class KmeansStats:
+    """kmeans.hpp:27-30."""
+    wcss: np.ndarray
+    iterations: int
+
+
+def kmeans_train(db, clusters: int, max_iters: int, seed: int = 42, ctx: Optional[Context] = None,
+                 stats: bool = False):
+    """kmeans.cpp:189-241 on the GPU (dvsg_kmeans_train): the reference's
+    k-means++ seeding (mt19937_64), Lloyd loop, empty-cluster repair and final
+    non-empty check.  -> centroids (clusters x dim), or (centroids, KmeansStats)."""
+    cx = ctx or default_context()
+    x = _f32(db, 2)
+    cents = np.zeros((max(int(clusters), 1), x.shape[1]), np.float32)
+    it = ctypes.c_int(0)
+    wcss = np.zeros(max(int(max_iters), 1), np.float64)
+    check(lib.dvsg_kmeans_train(cx.handle, _ptr(x), x.shape[0], x.shape[1], int(clusters), int(max_iters),
+                                ctypes.c_uint64(int(seed)), _ptr(cents), ctypes.byref(it), _ptr(wcss)))
+    return (cents, KmeansStats(wcss[:it.value].copy(), it.value)) if stats else cents
+
+
+def partition_database(db, centroids, ctx: Optional[Context] = None) -> List[np.ndarray]:
+    """kmeans.cpp:282-300: per cluster, the ids of its rows in row order."""
+    cx = ctx or default_context()
+    x = _f32(db, 2)
+    cents = _f32(centroids, 2)
+    if x.shape[1] != cents.shape[1]:
+        raise InvalidArgument("partition_database: dim mismatch")
+    lab = np.zeros(x.shape[0], np.uint32)
+    check(lib.dvsg_partition_database(cx.handle, _ptr(x), x.shape[0], x.shape[1], _ptr(cents), cents.shape[0],
+                                      _ptr(lab)))
+    order = np.argsort(lab, kind="stable")
+    bounds = np.searchsorted(lab[order], np.arange(cents.shape[0] + 1))
+    return [order[bounds[c]:bounds[c + 1]].astype(np.uint32) for c in range(cents.shape[0])]
+
+
+def build_index(db, clusters: int, out_degree: int, ranks: int = 1, kmeans_iters: int = 25, seed: int = 42,
+                ctx: Optional[Context] = None) -> BuiltIndex:
+    """index.cpp:43-72: kmeans_train -> place_clusters -> partition_database ->
+    one build_graph per cluster (GPU K6 on integer data, exact host rows
+    otherwise is the shim's job; this helper needs integer-valued data or an
+    approximation-tolerant caller)."""
+    cx = ctx or default_context()
+    x = _f32(db, 2)
+    if clusters < ranks:
+        raise InvalidArgument(f"build_index: clusters ({clusters}) must be >= ranks ({ranks})")
+    cents = kmeans_train(x, clusters, kmeans_iters, seed, ctx=cx)
+    placement = place_clusters(clusters, ranks)
+    graphs = []
+    for ids in partition_database(x, cents, ctx=cx):
+        part = np.ascontiguousarray(x[ids])
+        graphs.append(build_graph(part, out_degree, global_ids=ids, ctx=cx))
+    return BuiltIndex(cents, placement, ranks, out_degree, graphs)
 
 
 def place_clusters(clusters: int, ranks: int) -> np.ndarray:

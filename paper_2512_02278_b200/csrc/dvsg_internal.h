@@ -235,6 +235,19 @@ size_t graph_opt_scratch_bytes(uint64_t n, int d, int keep);
 cudaError_t launch_graph_optimize(uint32_t* adj, uint64_t n, int d, int keep, void* scratch,
                                   size_t scratch_bytes, cudaStream_t stream);
 
+// kmeans_train device parts (kmeans.cu)
+cudaError_t launch_kpp_d2(const float* x, uint64_t n, int dim, const float* center, double* d2, int first,
+                          cudaStream_t s);
+size_t kmeans_scan_bytes(uint64_t n);
+cudaError_t launch_kpp_scan(const double* d2, double* scan, uint64_t n, void* temp, size_t temp_bytes,
+                            cudaStream_t s);
+cudaError_t launch_first_gt(const double* scan, uint64_t n, double r, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_own_dist(const float* x, uint64_t n, int dim, const float* cents, const uint32_t* labels,
+                            float* out, cudaStream_t s);
+cudaError_t launch_cluster_means(const float* x, uint64_t n, int dim, const uint32_t* labels, int clusters,
+                                 float* cents, uint32_t* keys_tmp, uint32_t* order, uint32_t* iota,
+                                 void* temp, size_t temp_bytes, cudaStream_t s);
+
 // K6 exact kNN graph rows (knn_build.cu)
 cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad,
                              int out_degree, uint32_t* adjacency, cudaStream_t stream);

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <memory>
 #include <numeric>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -2045,6 +2046,223 @@ dvsg_status dvsg_index_integral(dvsg_ctx* c, int* out) {
   return guarded([&] {
     if (!out) fail(DVSG_EINVAL, "index_integral: null out");
     *out = c->all_integral ? 1 : 0;
+  });
+}
+
+// ---- kmeans_train / partition_database (kmeans.cpp:189-300) ---------------
+namespace {
+
+void validate_dataset(const float* x, uint64_t n, int dim) {
+  if (dim <= 0) fail(DVSG_EINVAL, "Dataset: dim must be positive, got %d", dim);
+  for (uint64_t i = 0; i < n * (uint64_t)dim; ++i)
+    if (!std::isfinite(x[i])) fail(DVSG_EINVAL, "Dataset: non-finite element at flat index %llu", (unsigned long long)i);
+}
+
+std::vector<double> center_norms(const std::vector<float>& cents, int clusters, int dim) {
+  std::vector<double> out((size_t)clusters);  // refresh_center_norms, kmeans.cpp:34-40
+  for (int j = 0; j < clusters; ++j) {
+    double acc = 0.0;
+    for (int i = 0; i < dim; ++i) {
+      const double v = (double)cents[(size_t)j * dim + i];
+      acc += v * v;
+    }
+    out[(size_t)j] = acc;
+  }
+  return out;
+}
+
+// nearest_center of every row (kmeans.cpp:50-82) == K5 top-1, in query chunks
+// that keep K5's (rows x clusters) key scratch under 512 MB
+void assign_nearest(dvsg_ctx* c, const float* d_x, uint64_t n, int dim, const float* d_cents,
+                    const double* d_norms, int clusters, uint32_t* d_labels, DevBuf<uint64_t>& scratch) {
+  const uint64_t chunk = std::max<uint64_t>(1024, (512ull << 20) / (8ull * (uint64_t)(clusters + 1)));
+  scratch.reserve(std::min<uint64_t>(chunk, n) * (uint64_t)(clusters + 1), c->stream);
+  for (uint64_t b = 0; b < n; b += chunk) {
+    const uint64_t m = std::min<uint64_t>(chunk, n - b);
+    cuda_check(dvsg::launch_assign(d_x + b * (uint64_t)dim, m, dim, d_cents, d_norms, clusters, 1, d_labels + b,
+                                   scratch.p, c->stream), "assign");
+    c->launches += 1;
+  }
+}
+
+}  // namespace
+
+dvsg_status dvsg_kmeans_train(dvsg_ctx* c, const float* db, uint64_t n, int dim, int clusters, int max_iters,
+                              uint64_t seed, float* centroids_out, int* iterations_out, double* wcss_out) {
+  return guarded([&] {
+    set_device(c);
+    validate_dataset(db, n, dim);
+    if (clusters < 1 || (uint64_t)clusters > n)
+      fail(DVSG_EINVAL, "kmeans_train: clusters=%d out of range for database of size %llu", clusters, (unsigned long long)n);
+    if (max_iters < 1) fail(DVSG_EINVAL, "kmeans_train: max_iters must be >= 1");
+    if (!centroids_out) fail(DVSG_EINVAL, "kmeans_train: null output");
+    cudaStream_t s = c->stream;
+    const size_t C = (size_t)clusters, D = (size_t)dim;
+    DevBuf<float> x, dc, od;
+    DevBuf<double> d2, scan, dn;
+    DevBuf<uint32_t> lab, keys, order, iota;
+    DevBuf<uint64_t> ascratch;
+    DevBuf<unsigned long long> pick;
+    DevBuf<unsigned char> temp;
+    x.reserve(n * D, s);
+    cuda_check(cudaMemcpyAsync(x.p, db, n * D * 4, cudaMemcpyHostToDevice, s), "db H2D");
+    dc.reserve(C * D, s);
+    d2.reserve(n, s);
+    scan.reserve(n, s);
+    lab.reserve(n, s);
+    od.reserve(n, s);
+    dn.reserve(C, s);
+    pick.reserve(1, s);
+    const size_t tb = dvsg::kmeans_scan_bytes(n);
+    temp.reserve(tb, s);
+    std::mt19937_64 rng(seed);
+    auto uniform01 = [&] { return (double)(rng() >> 11) * 0x1.0p-53; };
+    auto uniform_index = [&](uint64_t m) {
+      const uint64_t i = (uint64_t)(uniform01() * (double)m);
+      return i < m ? i : m - 1;
+    };
+    std::vector<float> cents(C * D);
+    auto set_center = [&](size_t j, uint64_t row) {
+      std::memcpy(cents.data() + j * D, db + row * D, D * 4);
+      cuda_check(cudaMemcpyAsync(dc.p + j * D, db + row * D, D * 4, cudaMemcpyHostToDevice, s), "center H2D");
+    };
+    // ---- init_kmeanspp (kmeans.cpp:150-187)
+    set_center(0, uniform_index(n));
+    cuda_check(dvsg::launch_kpp_d2(x.p, n, dim, dc.p, d2.p, 1, s), "kpp d2");
+    for (size_t j = 1; j < C; ++j) {
+      cuda_check(dvsg::launch_kpp_scan(d2.p, scan.p, n, temp.p, tb, s), "kpp scan");
+      double total = 0.0;
+      cuda_check(cudaMemcpyAsync(&total, scan.p + (n - 1), 8, cudaMemcpyDeviceToHost, s), "total");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+      uint64_t p;
+      if (total <= 0.0) {
+        p = uniform_index(n);  // all residual mass gone (duplicates)
+      } else {
+        const double r = uniform01() * total;
+        const unsigned long long init = n - 1;
+        cuda_check(cudaMemcpyAsync(pick.p, &init, 8, cudaMemcpyHostToDevice, s), "pick init");
+        cuda_check(dvsg::launch_first_gt(scan.p, n, r, pick.p, s), "first > r");
+        unsigned long long pk = 0;
+        cuda_check(cudaMemcpyAsync(&pk, pick.p, 8, cudaMemcpyDeviceToHost, s), "pick");
+        cuda_check(cudaStreamSynchronize(s), "sync");
+        p = pk;
+      }
+      set_center(j, p);
+      cuda_check(dvsg::launch_kpp_d2(x.p, n, dim, dc.p + j * D, d2.p, 0, s), "kpp d2");
+      c->launches += 3;
+    }
+    // ---- Lloyd (kmeans.cpp:216-226)
+    std::vector<uint32_t> labels(n), prev;
+    std::vector<float> dist(n);
+    auto assign_all = [&] {
+      const std::vector<double> norms = center_norms(cents, clusters, dim);
+      cuda_check(cudaMemcpyAsync(dn.p, norms.data(), C * 8, cudaMemcpyHostToDevice, s), "norms");
+      assign_nearest(c, x.p, n, dim, dc.p, dn.p, clusters, lab.p, ascratch);
+      cuda_check(cudaMemcpyAsync(labels.data(), lab.p, n * 4, cudaMemcpyDeviceToHost, s), "labels");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+    };
+    auto own_dists = [&] {
+      cuda_check(dvsg::launch_own_dist(x.p, n, dim, dc.p, lab.p, od.p, s), "own dist");
+      cuda_check(cudaMemcpyAsync(dist.data(), od.p, n * 4, cudaMemcpyDeviceToHost, s), "dists");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+      c->launches += 1;
+    };
+    // repair_empty_clusters (kmeans.cpp:84-117): every empty cluster takes the
+    // row farthest from its own centroid among clusters that can spare one
+    auto repair = [&] {
+      std::vector<uint64_t> sizes(C, 0);
+      for (uint32_t l : labels) ++sizes[l];
+      if (std::find(sizes.begin(), sizes.end(), 0ull) == sizes.end()) return false;
+      own_dists();  // unchanged by the moves below except for moved rows, which become ineligible
+      bool changed = false;
+      for (size_t e = 0; e < C; ++e) {
+        if (sizes[e] > 0) continue;
+        uint64_t worst = n;
+        float wd = -1.0f;
+        for (uint64_t i = 0; i < n; ++i) {
+          if (sizes[labels[i]] < 2) continue;
+          if (dist[i] > wd) {
+            wd = dist[i];
+            worst = i;
+          }
+        }
+        if (worst == n) {  // nothing movable: the reference returns false, keeping earlier moves
+          if (changed) cuda_check(cudaMemcpyAsync(lab.p, labels.data(), n * 4, cudaMemcpyHostToDevice, s), "labels H2D");
+          return false;
+        }
+        set_center(e, worst);
+        --sizes[labels[worst]];
+        labels[worst] = (uint32_t)e;
+        ++sizes[e];
+        changed = true;
+      }
+      if (changed) cuda_check(cudaMemcpyAsync(lab.p, labels.data(), n * 4, cudaMemcpyHostToDevice, s), "labels H2D");
+      return changed;
+    };
+    keys.reserve(n, s);
+    order.reserve(n, s);
+    iota.reserve(n, s);
+    int iters = 0;
+    for (int it = 0; it < max_iters; ++it) {
+      assign_all();
+      repair();
+      if (labels == prev) break;  // fixed point: means would not move
+      cuda_check(dvsg::launch_cluster_means(x.p, n, dim, lab.p, clusters, dc.p, keys.p, order.p, iota.p, temp.p, tb, s),
+                 "update means");
+      c->launches += 3;
+      cuda_check(cudaMemcpyAsync(cents.data(), dc.p, C * D * 4, cudaMemcpyDeviceToHost, s), "cents D2H");
+      if (wcss_out) {  // compute_wcss (kmeans.cpp:135-143): row-order fp64 sum
+        own_dists();
+        double acc = 0.0;
+        for (uint64_t i = 0; i < n; ++i) acc += (double)dist[i];
+        wcss_out[it] = acc;
+      } else {
+        cuda_check(cudaStreamSynchronize(s), "sync");
+      }
+      iters = it + 1;
+      prev = labels;
+    }
+    // the returned centroids must induce a partition with no empty cluster (:229-240)
+    for (int round = 0; round <= clusters; ++round) {
+      assign_all();
+      std::vector<char> seen(C, 0);
+      for (uint32_t l : labels) seen[l] = 1;
+      if (std::find(seen.begin(), seen.end(), 0) == seen.end()) {
+        std::memcpy(centroids_out, cents.data(), C * D * 4);
+        if (iterations_out) *iterations_out = iters;
+        return;
+      }
+      if (!repair()) break;
+    }
+    fail(DVSG_EINVAL, "kmeans_train: cannot keep %d clusters non-empty; the dataset has too few distinct points", clusters);
+  });
+}
+
+dvsg_status dvsg_partition_database(dvsg_ctx* c, const float* db, uint64_t n, int dim, const float* centroids,
+                                    int clusters, uint32_t* labels_out) {
+  return guarded([&] {
+    set_device(c);
+    validate_dataset(db, n, dim);
+    if (clusters < 1 || !centroids) fail(DVSG_EINVAL, "partition_database: empty centroids");
+    if (!labels_out) fail(DVSG_EINVAL, "partition_database: null output");
+    cudaStream_t s = c->stream;
+    std::vector<float> cents(centroids, centroids + (size_t)clusters * dim);
+    const std::vector<double> norms = center_norms(cents, clusters, dim);
+    DevBuf<float> x, dc;
+    DevBuf<double> dn;
+    DevBuf<uint32_t> lab;
+    DevBuf<uint64_t> scratch;
+    x.reserve(std::max<uint64_t>(n, 1) * (uint64_t)dim, s);
+    dc.reserve((size_t)clusters * dim, s);
+    dn.reserve((size_t)clusters, s);
+    lab.reserve(std::max<uint64_t>(n, 1), s);
+    if (n == 0) return;
+    cuda_check(cudaMemcpyAsync(x.p, db, n * (uint64_t)dim * 4, cudaMemcpyHostToDevice, s), "db H2D");
+    cuda_check(cudaMemcpyAsync(dc.p, centroids, (size_t)clusters * dim * 4, cudaMemcpyHostToDevice, s), "cents H2D");
+    cuda_check(cudaMemcpyAsync(dn.p, norms.data(), (size_t)clusters * 8, cudaMemcpyHostToDevice, s), "norms H2D");
+    assign_nearest(c, x.p, n, dim, dc.p, dn.p, clusters, lab.p, scratch);
+    cuda_check(cudaMemcpyAsync(labels_out, lab.p, n * 4, cudaMemcpyDeviceToHost, s), "labels D2H");
+    cuda_check(cudaStreamSynchronize(s), "sync");
   });
 }
 
