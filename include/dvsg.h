@@ -191,6 +191,34 @@ dvsg_status dvsg_set_shard_exchange(dvsg_ctx *ctx, int mode);
 dvsg_status dvsg_nccl_unique_id(dvsg_ctx *ctx, void *id_out128);
 dvsg_status dvsg_nccl_connect(dvsg_ctx *ctx, const void *id128);
 
+/* ---- cluster-sharded run_pipeline, device-initiated exchange ------------
+ * SURVEY 8e design A: cluster i lives on rank placement[i] (router.cpp:28-43),
+ * every rank holds the centroids + placement (dvsg_set_centroids) and its own
+ * partitions, and is the origin of its own query batch.  One call per step on
+ * every rank (collective, asynchronous on the compute stream): K5 assign ->
+ * K3 dispatch (each routed unit's query + header stored into the owner's
+ * inbox over NVLink, route router.cpp:52-79) -> peer-flag barrier -> K1 over
+ * the units this rank owns -> results (+ hit vectors) stored into each
+ * origin's reply slots -> barrier -> K4 combine_results (simulator.cpp:219-243)
+ * and the hit vectors (:329-333).  Results equal run_pipeline over the whole
+ * index on one GPU.  Replaces the NCCL all-to-alls of the Python driver. */
+dvsg_status dvsg_cluster_comm_init(dvsg_ctx *ctx, int nranks, int rank, uint64_t max_queries,
+                                   int max_fanout, int k, int with_vectors);
+/* 64-byte IPC handle of this rank's arena; connect with every rank's (rank order). */
+dvsg_status dvsg_cluster_comm_export(dvsg_ctx *ctx, void *handle_out);
+dvsg_status dvsg_cluster_comm_connect(dvsg_ctx *ctx, const void *handles);
+/* Same process, same device (tests): the arenas' device pointers directly. */
+void *dvsg_cluster_comm_arena(dvsg_ctx *ctx);
+dvsg_status dvsg_cluster_comm_connect_local(dvsg_ctx *ctx, void *const *arenas);
+dvsg_status dvsg_run_pipeline_cluster_device(dvsg_ctx *ctx, const float *d_queries, uint64_t nq,
+                                             int dim, const dvsg_search_params *p, int fanout,
+                                             uint32_t *d_out_ids, float *d_out_dists,
+                                             uint32_t *d_out_count, float *d_out_vectors,
+                                             uint64_t *d_visited_total);
+/* Synchronizes and reports an error of the last step (overflow, routing,
+ * barrier timeout, unsorted partial). */
+dvsg_status dvsg_cluster_comm_check(dvsg_ctx *ctx);
+
 /* ---- routing and merge -------------------------------------------------- */
 
 /* assign_top_c, kmeans.cpp:243-280, on the GPU against the context's

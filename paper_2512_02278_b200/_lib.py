@@ -108,6 +108,14 @@ _SIGS = {
     "dvsg_kmeans_train": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_int, c_uint64, c_void_p,
                                   POINTER(c_int), c_void_p]),
     "dvsg_partition_database": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p, c_int, c_void_p]),
+    "dvsg_cluster_comm_init": (c_int, [c_void_p, c_int, c_int, c_uint64, c_int, c_int, c_int]),
+    "dvsg_cluster_comm_export": (c_int, [c_void_p, c_void_p]),
+    "dvsg_cluster_comm_connect": (c_int, [c_void_p, c_void_p]),
+    "dvsg_cluster_comm_arena": (c_void_p, [c_void_p]),
+    "dvsg_cluster_comm_connect_local": (c_int, [c_void_p, c_void_p]),
+    "dvsg_run_pipeline_cluster_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, P_params, c_int, c_void_p,
+                                                 c_void_p, c_void_p, c_void_p, c_void_p]),
+    "dvsg_cluster_comm_check": (c_int, [c_void_p]),
     "dvsg_optimize_graph_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int]),
     "dvsg_partition_view_device": (c_int, [c_void_p, c_uint32, POINTER(c_void_p), POINTER(c_void_p),
                                            POINTER(c_void_p), POINTER(c_void_p), POINTER(c_uint64)]),

@@ -467,6 +467,41 @@ class Context:
     def optimize_graph_device(self, d_adjacency: int, n: int, out_degree: int, keep: int) -> None:
         check(lib.dvsg_optimize_graph_device(self._h, d_adjacency, int(n), int(out_degree), int(keep)))
 
+    # ---- cluster-sharded run_pipeline, device-initiated exchange -------------
+    def cluster_comm_init(self, nranks: int, rank: int, max_queries: int, max_fanout: int, k: int,
+                          with_vectors: bool = True) -> None:
+        check(lib.dvsg_cluster_comm_init(self._h, int(nranks), int(rank), int(max_queries), int(max_fanout),
+                                         int(k), int(bool(with_vectors))))
+
+    def cluster_comm_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        check(lib.dvsg_cluster_comm_export(self._h, buf))
+        return buf.raw
+
+    def cluster_comm_connect(self, handles) -> None:
+        blob = b"".join(handles)
+        check(lib.dvsg_cluster_comm_connect(self._h, ctypes.c_char_p(blob)))
+
+    def cluster_comm_arena(self) -> int:
+        return int(lib.dvsg_cluster_comm_arena(self._h) or 0)
+
+    def cluster_comm_connect_local(self, arenas) -> None:
+        arr = (ctypes.c_void_p * len(arenas))(*[int(a) for a in arenas])
+        check(lib.dvsg_cluster_comm_connect_local(self._h, arr))
+
+    def run_pipeline_cluster_device(self, d_queries: int, nq: int, dim: int, p: SearchParams, fanout: int,
+                                    d_ids: int, d_dists: int, d_counts: int, d_vectors: int = 0,
+                                    d_visited_total: int = 0) -> None:
+        cp = p.to_c()
+        check(lib.dvsg_run_pipeline_cluster_device(self._h, ctypes.c_void_p(d_queries), int(nq), int(dim),
+                                                   ctypes.byref(cp), int(fanout), ctypes.c_void_p(d_ids),
+                                                   ctypes.c_void_p(d_dists), ctypes.c_void_p(d_counts),
+                                                   ctypes.c_void_p(d_vectors or None),
+                                                   ctypes.c_void_p(d_visited_total or None)))
+
+    def cluster_comm_check(self) -> None:
+        check(lib.dvsg_cluster_comm_check(self._h))
+
     def index_integral(self) -> bool:
         out = ctypes.c_int()
         check(lib.dvsg_index_integral(self._h, ctypes.byref(out)))

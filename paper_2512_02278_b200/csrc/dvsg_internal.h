@@ -49,6 +49,7 @@ struct SearchArgs {
   uint64_t* out_visited;  // nunits
   unsigned long long* work_counter;
   unsigned long long* stats;  // [0] units, [1] visited, [2] expanded (frontier nodes); nullable
+  const unsigned long long* nunits_dev;  // nullable: unit count produced on the device (<= nunits)
 };
 
 // ---- node-sharded K1 (shard_kernel.cu) ------------------------------------
@@ -247,6 +248,39 @@ cudaError_t launch_own_dist(const float* x, uint64_t n, int dim, const float* ce
 cudaError_t launch_cluster_means(const float* x, uint64_t n, int dim, const uint32_t* labels, int clusters,
                                  float* cents, uint32_t* keys_tmp, uint32_t* order, uint32_t* iota,
                                  void* temp, size_t temp_bytes, cudaStream_t s);
+
+// ---- cluster-sharded run_pipeline exchange (cluster_xchg.cu) ---------------
+// Each rank's IPC-exported arena: header (barrier flags, per-origin inbox
+// cursors by step parity), its inbox (queries + {cluster, origin unit} of the
+// units other ranks route to it) and its reply region (per own unit: k ids,
+// k dists, count, visited, optional k hit vectors).
+struct ClArena {
+  unsigned* flags;        // [kXgMaxRanks] barrier epochs published by each rank
+  unsigned* cursor;       // [2][kXgMaxRanks] units written into this inbox by each origin, per parity
+  float* inbox_q;         // [R][cap][dim]
+  uint2* inbox_meta;      // [R][cap] {cluster, origin unit}
+  uint32_t* r_ids;        // [ucap][k]
+  float* r_dists;         // [ucap][k]
+  uint32_t* r_count;      // [ucap]
+  uint64_t* r_visited;    // [ucap]
+  float* r_vec;           // [ucap][k][dim] or null
+};
+cudaError_t launch_cl_dispatch(const ClArena* peers, int nranks, int me, int parity, const float* q, uint64_t nq,
+                               int dim, int fanout, const uint32_t* assign, const uint32_t* placement,
+                               uint32_t nclusters, uint64_t cap, int* err, cudaStream_t s);
+cudaError_t launch_cl_units(const ClArena* peers, int nranks, int me, int parity, uint64_t cap,
+                            const int32_t* cluster_to_slot, uint32_t nmap, uint32_t* unit_query,
+                            uint32_t* unit_part, unsigned long long* nunits, int* err, cudaStream_t s);
+cudaError_t launch_cl_reply(const ClArena* peers, int me, uint64_t cap, const uint32_t* unit_query,
+                            const unsigned long long* nunits, uint64_t max_units, int k, const uint32_t* ids,
+                            const float* dists, const uint32_t* counts, const uint64_t* visited,
+                            const uint64_t* locator, const float* vectors, int dim, int dpad, int with_vectors,
+                            cudaStream_t s);
+cudaError_t launch_cl_reset(const ClArena* peers, int me, int parity, cudaStream_t s);
+cudaError_t launch_cl_pick_vectors(const uint32_t* ids, const uint32_t* counts, uint64_t nq, int k, int fanout,
+                                   const uint32_t* r_ids, const uint32_t* r_count, const float* r_vec, int dim,
+                                   float* out, cudaStream_t s);
+cudaError_t launch_cl_barrier(const ClArena* peers, int nranks, int me, unsigned epoch, int* err, cudaStream_t s);
 
 // K6 exact kNN graph rows (knn_build.cu)
 cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad,

@@ -201,6 +201,25 @@ struct dvsg_ctx {
     bool issued = false;
   } xg;
 
+  // cluster-sharded run_pipeline exchange (cluster_xchg.cu): this rank's arena
+  struct Cl {
+    bool active = false, connected = false, with_vectors = false, own_peers = false;
+    int nranks = 0, rank = 0, k = 0, max_fanout = 0, dim = 0;
+    uint64_t max_queries = 0, cap = 0, ucap = 0;
+    size_t bytes = 0;
+    size_t off_q = 0, off_meta = 0, off_ids = 0, off_dists = 0, off_count = 0, off_vis = 0, off_vec = 0;
+    unsigned char* arena = nullptr;
+    std::vector<unsigned char*> peers;
+    unsigned epoch = 0;
+    int parity = 0;
+  } cl;
+  DevBuf<dvsg::ClArena> cl_peers;
+  DevBuf<uint32_t> cl_uq, cl_up, cl_ids, cl_count, cl_place;
+  DevBuf<float> cl_dists;
+  DevBuf<uint64_t> cl_vis;
+  DevBuf<unsigned long long> cl_nunits;
+  DevBuf<int> cl_err;
+
   // measured timeline of the last bulk-exchange search (timing on)
   std::vector<int> xg_tl;                      // 0: step kernel, 1: barrier / NCCL exchange
   std::vector<cudaEvent_t> xg_tl_ev;
@@ -418,7 +437,8 @@ dvsg::SearchArgs k1_args(dvsg_ctx* c, const dvsg_search_params* p, const K1Shape
 // Core: K1 over a device unit list.  All pointers device.
 void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uint32_t* d_uq,
                   const uint32_t* d_up, uint64_t nunits, const dvsg_search_params* p,
-                  uint32_t* d_ids, float* d_dists, uint32_t* d_count, uint64_t* d_visited) {
+                  uint32_t* d_ids, float* d_dists, uint32_t* d_count, uint64_t* d_visited,
+                  const unsigned long long* d_nunits = nullptr) {
   validate_params(p);
   const dvsg_search_params pe = effective_params(c, p);
   p = &pe;
@@ -432,6 +452,7 @@ void search_units(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const uin
   for (auto& pd : c->parts) nmax = std::max<uint64_t>(nmax, pd.n);
   const K1Shape k = k1_shape(c, p, nmax, true);
   dvsg::SearchArgs a = k1_args(c, p, k, d_q, nq, dim, d_uq, d_up, nunits, d_ids, d_dists, d_count, d_visited);
+  a.nunits_dev = d_nunits;  // unit count produced on the device (cluster exchange)
   // locality order: CTAs claim units grouped by the query's nearest anchor row,
   // so concurrent CTAs walk overlapping graph regions (L2 reuse).  Pure
   // scheduling: outputs are per unit, results are identical in any order.
@@ -1210,6 +1231,9 @@ dvsg_status dvsg_destroy(dvsg_ctx* c) {
     for (size_t r = 0; r < c->sh.peers.size(); ++r)
       if ((int)r != c->sh.rank && c->sh.peers[r]) cudaIpcCloseMemHandle(c->sh.peers[r]);
     if (c->sh.arena) cudaFree(c->sh.arena);
+    for (size_t r = 0; r < c->cl.peers.size(); ++r)
+      if ((int)r != c->cl.rank && c->cl.peers[r] && !c->cl.own_peers) cudaIpcCloseMemHandle(c->cl.peers[r]);
+    if (c->cl.arena) cudaFree(c->cl.arena);
     if (c->nccl) nccl_api().comm_destroy(c->nccl);
     for (auto& e : c->ev) cudaEventDestroy(e);
     for (auto& e : c->mb_ev) cudaEventDestroy(e);
@@ -2263,6 +2287,231 @@ dvsg_status dvsg_partition_database(dvsg_ctx* c, const float* db, uint64_t n, in
     assign_nearest(c, x.p, n, dim, dc.p, dn.p, clusters, lab.p, scratch);
     cuda_check(cudaMemcpyAsync(labels_out, lab.p, n * 4, cudaMemcpyDeviceToHost, s), "labels D2H");
     cuda_check(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+// ---- cluster-sharded run_pipeline with device-initiated exchange ----------
+namespace {
+
+size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
+constexpr size_t kClHeader = 4096;  // flags [8] u32 @0, cursor [2][8] u32 @64
+
+dvsg::ClArena cl_view(const dvsg_ctx* c, unsigned char* base) {
+  const auto& cl = c->cl;
+  dvsg::ClArena v{};
+  v.flags = reinterpret_cast<unsigned*>(base);
+  v.cursor = reinterpret_cast<unsigned*>(base + 64);
+  v.inbox_q = reinterpret_cast<float*>(base + cl.off_q);
+  v.inbox_meta = reinterpret_cast<uint2*>(base + cl.off_meta);
+  v.r_ids = reinterpret_cast<uint32_t*>(base + cl.off_ids);
+  v.r_dists = reinterpret_cast<float*>(base + cl.off_dists);
+  v.r_count = reinterpret_cast<uint32_t*>(base + cl.off_count);
+  v.r_visited = reinterpret_cast<uint64_t*>(base + cl.off_vis);
+  v.r_vec = cl.with_vectors ? reinterpret_cast<float*>(base + cl.off_vec) : nullptr;
+  return v;
+}
+
+void cl_connect(dvsg_ctx* c, const std::vector<unsigned char*>& bases) {
+  auto& cl = c->cl;
+  std::vector<dvsg::ClArena> views((size_t)cl.nranks);
+  for (int r = 0; r < cl.nranks; ++r) views[(size_t)r] = cl_view(c, bases[(size_t)r]);
+  c->cl_peers.reserve((size_t)cl.nranks, c->stream);
+  cuda_check(cudaMemcpyAsync(c->cl_peers.p, views.data(), views.size() * sizeof(dvsg::ClArena), cudaMemcpyHostToDevice, c->stream), "peers");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  cl.peers = bases;
+  cl.connected = true;
+}
+
+void cl_check(dvsg_ctx* c) {
+  if (!c->cl.active || !c->cl_err.p) return;
+  int flag = 0, comb = 0;
+  cuda_check(cudaMemcpyAsync(&flag, c->cl_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "cl err");
+  if (c->err_flag.p) cuda_check(cudaMemcpyAsync(&comb, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "err");
+  cuda_check(cudaStreamSynchronize(c->stream), "sync");
+  if (!flag && !comb) return;
+  cuda_check(cudaMemsetAsync(c->cl_err.p, 0, sizeof(int), c->stream), "cl err reset");
+  if (c->err_flag.p) cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+  if (flag & 1) fail(DVSG_EINTERNAL, "cluster exchange: a query was assigned a cluster id outside the routing table");
+  if (flag & 2) fail(DVSG_EINVAL, "cluster exchange: an owner's inbox overflowed (raise max_queries/max_fanout)");
+  if (flag & 4) fail(DVSG_EINTERNAL, "cluster exchange: a unit was routed to a rank that does not hold its cluster");
+  if (flag & 8) fail(DVSG_EINTERNAL, "cluster exchange: a rank did not reach the barrier within 20 s");
+  fail(DVSG_EINTERNAL, "combine_results: partial result list is not sorted");
+}
+
+}  // namespace
+
+dvsg_status dvsg_cluster_comm_init(dvsg_ctx* c, int nranks, int rank, uint64_t max_queries, int max_fanout, int k,
+                                   int with_vectors) {
+  return guarded([&] {
+    set_device(c);
+    if (nranks < 1 || nranks > dvsg::kXgMaxRanks || rank < 0 || rank >= nranks)
+      fail(DVSG_EINVAL, "cluster_comm_init: rank %d of %d", rank, nranks);
+    if (c->dim < 1) fail(DVSG_EINVAL, "cluster_comm_init: load this rank's partitions and centroids first");
+    if (max_queries < 1 || max_fanout < 1 || max_fanout > 32 || k < 1)
+      fail(DVSG_EINVAL, "cluster_comm_init: bad capacity (max_queries %llu, max_fanout %d, k %d)",
+           (unsigned long long)max_queries, max_fanout, k);
+    auto& cl = c->cl;
+    for (size_t r = 0; r < cl.peers.size(); ++r)
+      if ((int)r != cl.rank && cl.peers[r] && !cl.own_peers) cudaIpcCloseMemHandle(cl.peers[r]);
+    if (cl.arena) cudaFree(cl.arena);
+    cl = dvsg_ctx::Cl{};
+    cl.nranks = nranks;
+    cl.rank = rank;
+    cl.k = k;
+    cl.max_fanout = max_fanout;
+    cl.max_queries = max_queries;
+    cl.dim = c->dim;
+    cl.with_vectors = with_vectors != 0;
+    cl.cap = max_queries * (uint64_t)max_fanout;  // worst case: every unit of an origin to one owner
+    cl.ucap = cl.cap;
+    size_t o = kClHeader;
+    cl.off_q = o;
+    o = al256(o + (size_t)nranks * cl.cap * (size_t)c->dim * 4);
+    cl.off_meta = o;
+    o = al256(o + (size_t)nranks * cl.cap * 8);
+    cl.off_ids = o;
+    o = al256(o + cl.ucap * (size_t)k * 4);
+    cl.off_dists = o;
+    o = al256(o + cl.ucap * (size_t)k * 4);
+    cl.off_count = o;
+    o = al256(o + cl.ucap * 4);
+    cl.off_vis = o;
+    o = al256(o + cl.ucap * 8);
+    cl.off_vec = o;
+    if (cl.with_vectors) o = al256(o + cl.ucap * (size_t)k * (size_t)c->dim * 4);
+    cl.bytes = o;
+    cuda_check(cudaMalloc(&cl.arena, cl.bytes), "cluster arena");
+    cuda_check(cudaMemset(cl.arena, 0, kClHeader), "cluster arena header");
+    const uint64_t units = (uint64_t)nranks * cl.cap;
+    c->cl_uq.reserve(units, c->stream);
+    c->cl_up.reserve(units, c->stream);
+    c->cl_ids.reserve(units * (uint64_t)k, c->stream);
+    c->cl_dists.reserve(units * (uint64_t)k, c->stream);
+    c->cl_count.reserve(units, c->stream);
+    c->cl_vis.reserve(units, c->stream);
+    c->cl_nunits.reserve(1, c->stream);
+    c->cl_err.reserve(1, c->stream);
+    cuda_check(cudaMemset(c->cl_err.p, 0, sizeof(int)), "err");
+    std::vector<uint32_t> place(c->placement.begin(), c->placement.end());
+    if (place.empty()) fail(DVSG_EINVAL, "cluster_comm_init: no routing table (dvsg_set_centroids)");
+    for (uint32_t r : place)
+      if ((int)r >= nranks) fail(DVSG_EINVAL, "cluster_comm_init: placement names rank %u of %d", r, nranks);
+    c->cl_place.reserve(place.size(), c->stream);
+    cuda_check(cudaMemcpy(c->cl_place.p, place.data(), place.size() * 4, cudaMemcpyHostToDevice), "placement");
+    cl.active = true;
+  });
+}
+
+dvsg_status dvsg_cluster_comm_export(dvsg_ctx* c, void* handle_out) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->cl.active) fail(DVSG_EINVAL, "cluster_comm_export: call dvsg_cluster_comm_init first");
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, c->cl.arena), "ipc handle");
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+
+dvsg_status dvsg_cluster_comm_connect(dvsg_ctx* c, const void* handles) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->cl.active) fail(DVSG_EINVAL, "cluster_comm_connect: call dvsg_cluster_comm_init first");
+    std::vector<unsigned char*> bases((size_t)c->cl.nranks, nullptr);
+    for (int r = 0; r < c->cl.nranks; ++r) {
+      if (r == c->cl.rank) {
+        bases[(size_t)r] = c->cl.arena;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const unsigned char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+      void* p = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "ipc open");
+      bases[(size_t)r] = static_cast<unsigned char*>(p);
+    }
+    c->cl.own_peers = false;
+    cl_connect(c, bases);
+  });
+}
+
+void* dvsg_cluster_comm_arena(dvsg_ctx* c) { return c && c->cl.active ? c->cl.arena : nullptr; }
+
+dvsg_status dvsg_cluster_comm_connect_local(dvsg_ctx* c, void* const* arenas) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->cl.active) fail(DVSG_EINVAL, "cluster_comm_connect: call dvsg_cluster_comm_init first");
+    std::vector<unsigned char*> bases((size_t)c->cl.nranks);
+    for (int r = 0; r < c->cl.nranks; ++r) bases[(size_t)r] = static_cast<unsigned char*>(arenas[r]);
+    c->cl.own_peers = true;
+    cl_connect(c, bases);
+  });
+}
+
+dvsg_status dvsg_run_pipeline_cluster_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim,
+                                             const dvsg_search_params* p, int fanout, uint32_t* d_ids,
+                                             float* d_dists, uint32_t* d_count, float* d_vectors,
+                                             uint64_t* d_visited_total) {
+  return guarded([&] {
+    set_device(c);
+    auto& cl = c->cl;
+    if (!cl.active || !cl.connected) fail(DVSG_EINVAL, "cluster exchange: call dvsg_cluster_comm_init / connect first");
+    cl_check(c);  // errors of the previous step
+    validate_params(p);
+    if (dim != c->dim) fail(DVSG_EINVAL, "run_pipeline: query dim %d != index dim %d", dim, c->dim);
+    if (fanout < 1 || fanout > c->clusters)
+      fail(DVSG_EINVAL, "run_pipeline: fanout %d out of range for %d clusters", fanout, c->clusters);
+    if (fanout > cl.max_fanout || nq > cl.max_queries || p->k != cl.k)
+      fail(DVSG_EINVAL, "cluster exchange: batch (nq %llu, fanout %d, k %d) exceeds the arena (%llu, %d, %d)",
+           (unsigned long long)nq, fanout, p->k, (unsigned long long)cl.max_queries, cl.max_fanout, cl.k);
+    if (d_vectors && !cl.with_vectors) fail(DVSG_EINVAL, "cluster exchange: arena built without hit vectors");
+    sync_slots(c);
+    if (cl.with_vectors) build_locator(c);
+    const dvsg::ClArena mine = cl_view(c, cl.arena);
+    const uint64_t nu = nq * (uint64_t)fanout;
+    cudaStream_t s = c->stream;
+    c->err_flag.reserve(1, s);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), s), "err reset");
+    // assign (K5) -> dispatch (K3, peer stores) -> barrier
+    c->assign.reserve(std::max<uint64_t>(nu, 1), s);
+    c->assign_scratch.reserve(std::max<uint64_t>(nq, 1) * ((uint64_t)c->clusters + 1), s);
+    if (nq) cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout,
+                                           c->assign.p, c->assign_scratch.p, s), "assign");
+    cuda_check(dvsg::launch_cl_dispatch(c->cl_peers.p, cl.nranks, cl.rank, cl.parity, d_q, nq, dim, fanout,
+                                        c->assign.p, c->cl_place.p, (uint32_t)c->clusters, cl.cap, c->cl_err.p, s),
+               "dispatch");
+    cuda_check(dvsg::launch_cl_barrier(c->cl_peers.p, cl.nranks, cl.rank, ++cl.epoch, c->cl_err.p, s), "barrier");
+    cuda_check(dvsg::launch_cl_reset(c->cl_peers.p, cl.rank, cl.parity, s), "reset");
+    // owner: the units in this rank's inbox -> K1 -> replies (peer stores) -> barrier
+    cuda_check(dvsg::launch_cl_units(c->cl_peers.p, cl.nranks, cl.rank, cl.parity, cl.cap, c->d_cluster_slot.p,
+                                     c->slot_map_n, c->cl_uq.p, c->cl_up.p, c->cl_nunits.p, c->cl_err.p, s), "units");
+    const uint64_t max_units = (uint64_t)cl.nranks * cl.cap;
+    search_units(c, mine.inbox_q, max_units, dim, c->cl_uq.p, c->cl_up.p, max_units, p, c->cl_ids.p,
+                 c->cl_dists.p, c->cl_count.p, c->cl_vis.p, c->cl_nunits.p);
+    cuda_check(dvsg::launch_cl_reply(c->cl_peers.p, cl.rank, cl.cap, c->cl_uq.p, c->cl_nunits.p, max_units, p->k,
+                                     c->cl_ids.p, c->cl_dists.p, c->cl_count.p, c->cl_vis.p,
+                                     cl.with_vectors ? c->d_locator.p : nullptr, c->vec.p, dim, c->dpad,
+                                     cl.with_vectors ? 1 : 0, s), "reply");
+    cuda_check(dvsg::launch_cl_barrier(c->cl_peers.p, cl.nranks, cl.rank, ++cl.epoch, c->cl_err.p, s), "barrier");
+    // origin: combine (K4) over the replies in unit order, hit vectors, visited_total
+    if (nq) {
+      cuda_check(dvsg::launch_combine(nq, fanout, mine.r_ids, mine.r_dists, mine.r_count, p->k, p->k, d_ids, d_dists,
+                                      d_count, c->err_flag.p, s), "combine");
+      if (d_vectors)
+        cuda_check(dvsg::launch_cl_pick_vectors(d_ids, d_count, nq, p->k, fanout, mine.r_ids, mine.r_count,
+                                                mine.r_vec, dim, d_vectors, s), "pick vectors");
+      if (d_visited_total) {
+        cuda_check(cudaMemsetAsync(d_visited_total, 0, 8, s), "visited reset");
+        cuda_check(dvsg::launch_reduce_u64(mine.r_visited, nu, reinterpret_cast<unsigned long long*>(d_visited_total), s), "visited");
+      }
+    }
+    c->launches += 9;
+    cl.parity ^= 1;
+  });
+}
+
+dvsg_status dvsg_cluster_comm_check(dvsg_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    cl_check(c);
   });
 }
 

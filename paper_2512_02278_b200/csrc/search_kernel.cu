@@ -74,14 +74,15 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   const unsigned full = 0xFFFFFFFFu;
   const unsigned lt_mask = (1u << lane) - 1u;
 
+  const uint64_t nunits = a.nunits_dev ? (uint64_t)*a.nunits_dev : a.nunits;
   for (;;) {
     if (tid == 0) {
       const unsigned long long ticket = atomicAdd(a.work_counter, 1ull);
-      st.unit = (a.unit_order && ticket < a.nunits) ? a.unit_order[ticket] : ticket;
+      st.unit = (a.unit_order && ticket < nunits) ? a.unit_order[ticket] : ticket;
     }
     __syncthreads();
     const uint64_t unit = st.unit;
-    if (unit >= a.nunits) return;
+    if (unit >= nunits) return;
 
     const uint32_t qi = a.unit_query[unit];
     const PartDesc part = a.parts[a.unit_part[unit]];

@@ -65,6 +65,35 @@ def setup_sharded_resident(ctx, rank: int, nranks: int, group=None,
     ctx.shard_connect(handles)
 
 
+def setup_cluster_comm(ctx, rank: int, world: int, max_queries: int, max_fanout: int, k: int,
+                       with_vectors: bool = True, group=None, exchange=exchange_handles) -> None:
+    """Arena of the device-initiated cluster exchange (cluster_xchg.cu); ctx
+    already holds this rank's partitions and the routing table."""
+    ctx.cluster_comm_init(world, rank, max_queries, max_fanout, k, with_vectors)
+    ctx.cluster_comm_connect(exchange(ctx.cluster_comm_export(), group))
+
+
+def run_pipeline_cluster(ctx, d_q, p, fanout: int, with_vectors: bool = True):
+    """run_pipeline (simulator.cpp:250-337), cluster-sharded, with the
+    dispatch / combine done by the library's own peer-store kernels (K3/K4) --
+    no NCCL collective and no host round trip.  Collective: every rank calls
+    it for its own batch.  -> torch tensors (ids, dists, counts, vectors or
+    None, visited_total as a 1-element int64 tensor), asynchronous on ctx.stream."""
+    import torch
+    dev = d_q.device
+    nq, dim = int(d_q.shape[0]), int(d_q.shape[1])
+    k = int(p.k)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    counts = torch.empty((nq,), dtype=torch.int32, device=dev)
+    vecs = torch.zeros((nq, k, dim), dtype=torch.float32, device=dev) if with_vectors else None
+    vt = torch.zeros(1, dtype=torch.int64, device=dev)
+    torch.cuda.current_stream(dev).synchronize()  # d_q / outputs ready before the library stream uses them
+    ctx.run_pipeline_cluster_device(d_q.data_ptr(), nq, dim, p, fanout, ids.data_ptr(), dists.data_ptr(),
+                                    counts.data_ptr(), vecs.data_ptr() if with_vectors else 0, vt.data_ptr())
+    return ids, dists, counts, vecs, vt
+
+
 def connect_nccl(ctx, rank: int, group=None) -> None:
     """NCCL communicator for the 'nccl' exchange: rank 0's unique id is
     broadcast over torch.distributed (control plane only)."""

@@ -90,6 +90,36 @@ def main():
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # the library's own device-initiated exchange (cluster_xchg.cu: K3 dispatch
+    # by peer stores, K1, results back by peer stores, K4 combine; no NCCL, no
+    # host round trip)
+    from paper_2512_02278_b200.dist import run_pipeline_cluster, setup_cluster_comm
+    setup_cluster_comm(ctx, rank, world, a.nq, a.fanout, 10, True)
+    nat = run_pipeline_cluster(ctx, torch.from_numpy(qc).to(dev), p, a.fanout)
+    ctx.synchronize()
+    ctx.cluster_comm_check()
+    ok_n = bool(np.array_equal(nat[2].cpu().numpy().view(np.uint32), want.counts)
+                and int(nat[4][0]) == want.visited_total
+                and np.array_equal(nat[0].cpu().numpy().view(np.uint32), gi)
+                and np.array_equal(nat[1].cpu().numpy(), gd) and np.array_equal(nat[3].cpu().numpy(), gv))
+    same_n = torch.tensor([int(ok_n)], device=dev)
+    dist.all_reduce(same_n, op=dist.ReduceOp.MIN)
+    for _ in range(2):
+        run_pipeline_cluster(ctx, d_q, p, a.fanout)
+    ctx.synchronize()
+    dist.barrier()
+    n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0.record(stream)
+    for _ in range(a.steps):
+        run_pipeline_cluster(ctx, d_q, p, a.fanout)
+    n1.record(stream)
+    ctx.synchronize()
+    ctx.cluster_comm_check()
+    tn = torch.tensor([n0.elapsed_time(n1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+    native = {"qps": a.nq * world / (float(tn[0]) / a.steps / 1e3), "ms_per_step": float(tn[0]) / a.steps,
+              "identical_to_one_gpu_pipeline_all_ranks": bool(same_n[0]),
+              "exchange": "library peer-store dispatch/combine (cluster_xchg.cu), device-side unit counts"}
     # the microbatched schedule (dispatch / combine overlapping search)
     from paper_2512_02278_b200.dist import run_pipeline_distributed_mb
     cctx = dvs.Context(local)
@@ -134,7 +164,7 @@ def main():
             "qps": a.nq * world / (ms / 1e3), "ms_per_step": ms, "visited_per_query": vis / a.steps / a.nq,
             "recall_at_10_rank0": round(rec, 4), "identical_to_one_gpu_pipeline_all_ranks": bool(same[0]),
             "checked_queries_per_rank": a.check, "setup_s": round(setup_s, 1),
-            "microbatched": mb_out,
+            "microbatched": mb_out, "native_exchange": native,
             "exchange": "NCCL all_to_all_single (torch.distributed): dispatch of (query, cluster) units, "
                         "results + hit vectors back"}), flush=True)
     dist.destroy_process_group()
