@@ -43,6 +43,9 @@ namespace {
 #ifndef DVSG_K1_BATCH_PROBES
 #define DVSG_K1_BATCH_PROBES 0  // measured: batched probe rounds -4%
 #endif
+#ifndef DVSG_K1_WARP_FUSED
+#define DVSG_K1_WARP_FUSED 0  // 1: each warp scores the new ids it probed (no block barrier between)
+#endif
 #ifndef DVSG_K1_SORT_RUNS
 #define DVSG_K1_SORT_RUNS 0
 #endif
@@ -246,6 +249,9 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           }
         }
 #endif
+#if DVSG_K1_WARP_FUSED
+        int wcount = 0;
+#endif
 #pragma unroll
         for (int j = 0; j < kRawPerThread; ++j) {
           if (j * kThreads >= rcount) break;  // block-uniform
@@ -273,36 +279,51 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
                                                                    : visit_insert(table, hmask, ids[j]));
 #endif
           const unsigned bal = __ballot_sync(full, isnew);
+#if DVSG_K1_WARP_FUSED
+          // warp-local list: this warp scores its own new ids right away
+          if (isnew) cand[warp * (kRawPerThread * 32) + wcount + __popc(bal & lt_mask)] = ids[j];
+          wcount += __popc(bal);
+#else
           int base = 0;
           if (lane == 0 && bal) base = atomicAdd(&st.ncand, __popc(bal));
           base = __shfl_sync(full, base, 0);
           if (isnew) cand[base + __popc(bal & lt_mask)] = ids[j];
+#endif
         }
+#if DVSG_K1_WARP_FUSED
+        if (lane == 0 && wcount) atomicAdd(&st.ncand, wcount);
+        __syncwarp();
+        const uint32_t* clist = cand + warp * (kRawPerThread * 32);
+        const int Mlim = wcount, cb0 = 0, cstep = U;
+#else
         __syncthreads();
         const int M = st.ncand;
         visited += (uint64_t)M;
+        const uint32_t* clist = cand;
+        const int Mlim = M, cb0 = warp * U, cstep = kWarps * U;
+#endif
 
         // ---- score new candidates: warp per vector, U vectors in flight per warp
 #if DVSG_SCORE_ROLLED
 #pragma unroll 1
 #endif
-        for (int cb = warp * U; cb < M; cb += kWarps * U) {
+        for (int cb = cb0; cb < Mlim; cb += cstep) {
           uint32_t ids_u[U];
           if constexpr (U >= 4) {
 #pragma unroll
             for (int u4 = 0; u4 < U; u4 += 4) {
-              const uint4 w4 = *reinterpret_cast<const uint4*>(cand + cb + u4);
+              const uint4 w4 = *reinterpret_cast<const uint4*>(clist + cb + u4);
               ids_u[u4] = w4.x; ids_u[u4 + 1] = w4.y; ids_u[u4 + 2] = w4.z; ids_u[u4 + 3] = w4.w;
             }
           } else {
 #pragma unroll
-            for (int u = 0; u < U; ++u) ids_u[u] = cand[cb + u];
+            for (int u = 0; u < U; ++u) ids_u[u] = clist[cb + u];
           }
           float4 x[U][VPL];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             // past M: load row 0 (harmless, result discarded by the ci < M test)
-            const uint32_t id = cb + u < M ? ids_u[u] : 0u;
+            const uint32_t id = cb + u < Mlim ? ids_u[u] : 0u;
             const float* row = lbase + (uint64_t)id * rstride;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -324,9 +345,9 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           const int ci = cb + myu;
           bool pass = false;
           uint64_t mykey = 0;
-          if ((lane & ((32 >> LU) - 1)) == 0 && ci < M) {
+          if ((lane & ((32 >> LU) - 1)) == 0 && ci < Mlim) {
             const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
-            mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
+            mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)clist[ci] << 1);
             pass = mykey < thresh;
           }
           const unsigned bal = __ballot_sync(full, pass);
@@ -337,6 +358,9 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
         }
         __syncthreads();
         const int S = st.nsurv;
+#if DVSG_K1_WARP_FUSED
+        visited += (uint64_t)st.ncand;
+#endif
         __syncthreads();  // every thread has read the counters before the next reset
         if (S == 0) continue;  // block-uniform
 
