@@ -43,6 +43,9 @@ namespace {
 #ifndef DVSG_K1_BATCH_PROBES
 #define DVSG_K1_BATCH_PROBES 0  // measured: batched probe rounds -4%
 #endif
+#ifndef DVSG_K1_TMA_GATHER
+#define DVSG_K1_TMA_GATHER 0  // 1: candidate rows staged in smem by cp.async.bulk (mbarrier completion)
+#endif
 #ifndef DVSG_K1_WARP_FUSED
 #define DVSG_K1_WARP_FUSED 0  // 1: each warp scores the new ids it probed (no block barrier between)
 #endif
@@ -52,6 +55,37 @@ namespace {
 
 // VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
 // FULL: dpad == 128 * VPL (every lane holds real dimensions; no bound check).
+#if DVSG_K1_TMA_GATHER
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+#endif
+
 template <int VPL, typename ACC, int METRIC, bool FULL>
 #ifndef DVSG_MINB
 #define DVSG_MINB 5  // resident CTAs per SM the register budget is cut for (measured sweep)
@@ -76,6 +110,18 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   const uint32_t dg_magic = (uint32_t)((0x100000000ull + (uint64_t)a.dg - 1) / (uint64_t)a.dg);
   const unsigned full = 0xFFFFFFFFu;
   const unsigned lt_mask = (1u << lane) - 1u;
+#if DVSG_K1_TMA_GATHER
+  // per-warp staging (U rows, <= 4 KB) + one mbarrier per warp, at the end
+  // of the dynamic smem (search_smem_bytes adds them)
+  uint32_t* const smem_end = frontier + ((a.beam + 3) & ~3) + (a.hash_global ? 0 : a.hsize);
+  float* const tma_stage = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(smem_end) + 15) & ~(uintptr_t)15) + warp * 1024;
+  uint64_t* const tma_bar = reinterpret_cast<uint64_t*>(tma_stage - warp * 1024 + kWarps * 1024) + warp;
+  unsigned tma_phase = 0;
+  if (lane == 0) mbar_init(tma_bar, 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+#endif
 
   const uint64_t nunits = a.nunits_dev ? (uint64_t)*a.nunits_dev : a.nunits;
   for (;;) {
@@ -320,6 +366,31 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
             for (int u = 0; u < U; ++u) ids_u[u] = clist[cb + u];
           }
           float4 x[U][VPL];
+#if DVSG_K1_TMA_GATHER
+          {
+            // lane 0 issues one bulk copy per row into the warp's staging
+            // buffer; every lane waits on the mbarrier, then reads its slices
+            const unsigned rowb = (unsigned)a.dpad * 4u;
+            const int nv = Mlim - cb < U ? Mlim - cb : U;
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              mbar_expect_tx(tma_bar, rowb * (unsigned)nv);
+#pragma unroll
+              for (int u = 0; u < U; ++u)
+                if (u < nv) bulk_g2s(tma_stage + u * a.dpad, vbase + (uint64_t)ids_u[u] * rstride, rowb, tma_bar);
+            }
+            mbar_wait(tma_bar, tma_phase);
+            tma_phase ^= 1u;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+              for (int v = 0; v < VPL; ++v)
+                x[u][v] = (u < nv && (FULL || lane * 4 + 128 * v < a.dpad))
+                              ? *reinterpret_cast<const float4*>(tma_stage + u * a.dpad + lane * 4 + 128 * v)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#else
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             // past M: load row 0 (harmless, result discarded by the ci < M test)
@@ -331,6 +402,7 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
               else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
+#endif
           ACC part[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -481,6 +553,9 @@ size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_sme
   size_t b = sizeof(uint64_t) * (2 * (size_t)cap + (size_t)chp);
   b += sizeof(uint32_t) * ((size_t)kChunk + (size_t)((beam + 3) & ~3));
   if (hash_in_smem) b += sizeof(uint32_t) * (size_t)hsize;
+#if DVSG_K1_TMA_GATHER
+  b = ((b + 15) & ~(size_t)15) + (size_t)kWarps * 4096 + (size_t)kWarps * 8 + 16;
+#endif
   return b;
 }
 
