@@ -243,7 +243,8 @@ def build_cfg3(args, rank, ctx, dev, gt_rows=None):
     else:
         x = ivf.sift_like_device(args.n, args.dim, args.rank_latent, seed=1, device=dev, dpad=dpad)
     info = ivf.build_graph_ivf(ctx, x, degree=args.degree, cluster_size=args.cluster_size, probe=args.probe,
-                               dim=args.dim, optimize=True, keep=args.keep, log=log)
+                               dim=args.dim, optimize=True, keep=args.keep,
+                               tensor_cores=args.metric == "l2", log=log)  # byte data: tcgen05 K7 is exact
     del x
     info.pop("perm")
     torch.cuda.empty_cache()
@@ -263,7 +264,9 @@ def build_cfg3(args, rank, ctx, dev, gt_rows=None):
     else:
         q = ivf.sift_like_queries_device(args.nq, args.dim, args.rank_latent, data_seed=1, seed=2 + rank,
                                          device=dev)
-        gt, _ = ivf.brute_force_topk(ctx, vec, ivf.row_norms(ctx, vec), q[:s].contiguous(), args.k)
+        vb = ivf.to_bf16(ctx, vec)  # ground truth on the tensor cores (exact on byte data)
+        gt, _ = ivf.brute_force_topk(ctx, vec, ivf.row_norms(ctx, vec), q[:s].contiguous(), args.k, db_bf16=vb)
+        del vb
     w = Workload()
     w.queries = q
     w.gt = gt.cpu().numpy()

@@ -332,6 +332,20 @@ dvsg_status dvsg_range_topk_device(dvsg_ctx *ctx, const float *d_rows, const flo
                                    const uint32_t *d_list_off, const uint32_t *d_ranges, int m,
                                    int flags, uint32_t *d_out_ids, float *d_out_dists,
                                    uint64_t out_stride);
+/* K7 on the tensor cores (csrc/ivf_tc.cu): the same contract over bf16 rows /
+ * columns (n x kpad, kpad a multiple of 16 <= 256, zero pad), one
+ * tcgen05.mma (M=128, N=128, K=16) per K slice into TMEM, top-m epilogue
+ * from tcgen05.ld.  Exact (== dvsg_range_topk_device) when the data are
+ * integers in [-256, 256] (bf16-exact, every fp32 partial sum exact). */
+dvsg_status dvsg_range_topk_bf16_device(dvsg_ctx *ctx, const uint16_t *d_rows, const float *d_row_norms,
+                                        const uint16_t *d_cols, const float *d_col_norms, int kpad,
+                                        const uint32_t *d_row_map, const dvsg_range_block *d_blocks,
+                                        uint64_t nblocks, const uint32_t *d_list_off,
+                                        const uint32_t *d_ranges, int m, int flags, uint32_t *d_out_ids,
+                                        float *d_out_dists, uint64_t out_stride);
+/* n rows of dpad floats -> n rows of kpad bf16 (round to nearest even, zero pad) */
+dvsg_status dvsg_to_bf16_device(dvsg_ctx *ctx, const float *d_x, uint64_t n, int dpad, int kpad,
+                                uint16_t *d_out);
 /* fp32 squared norms of n rows of dpad floats */
 dvsg_status dvsg_row_norms_device(dvsg_ctx *ctx, const float *d_x, uint64_t n, int dpad,
                                   float *d_out);

@@ -99,6 +99,10 @@ _SIGS = {
     "dvsg_range_topk_device": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                                        c_void_p, c_uint64, c_void_p, c_void_p, c_int, c_int, c_void_p,
                                        c_void_p, c_uint64]),
+    "dvsg_to_bf16_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
+    "dvsg_range_topk_bf16_device": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
+                                            c_void_p, c_uint64, c_void_p, c_void_p, c_int, c_int, c_void_p,
+                                            c_void_p, c_uint64]),
     "dvsg_segment_means_device": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_uint32, c_void_p]),
     "dvsg_compute_entry_order_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_int, c_void_p]),
     "dvsg_partition_alloc_device": (c_int, [c_void_p, c_uint32, c_uint64, c_int, c_int, POINTER(c_void_p),

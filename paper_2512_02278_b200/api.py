@@ -437,6 +437,17 @@ class Context:
                                          d_ranges or None, m, flags, d_out_ids, d_out_dists or None,
                                          out_stride))
 
+    def to_bf16_device(self, d_x: int, n: int, dpad: int, kpad: int, d_out: int) -> None:
+        check(lib.dvsg_to_bf16_device(self._h, d_x, n, dpad, kpad, d_out))
+
+    def range_topk_bf16_device(self, d_rows: int, d_row_norms: int, d_cols: int, d_col_norms: int, kpad: int,
+                               d_row_map: int, d_blocks: int, nblocks: int, d_list_off: int, d_ranges: int,
+                               m: int, flags: int, d_out_ids: int, d_out_dists: int, out_stride: int) -> None:
+        check(lib.dvsg_range_topk_bf16_device(self._h, d_rows, d_row_norms, d_cols, d_col_norms, kpad,
+                                              d_row_map or None, d_blocks or None, nblocks, d_list_off or None,
+                                              d_ranges or None, m, flags, d_out_ids, d_out_dists or None,
+                                              out_stride))
+
     def segment_means_device(self, d_x: int, dpad: int, d_idx: int, d_off: int, nseg: int,
                              d_cents: int) -> None:
         check(lib.dvsg_segment_means_device(self._h, d_x, dpad, d_idx or None, d_off, nseg, d_cents))

@@ -216,6 +216,13 @@ cudaError_t launch_range_topk(const float* rows, const float* rnorm, const float
                               int m, int flags, uint32_t* out_ids, float* out_dists,
                               uint64_t out_stride, cudaStream_t stream);
 size_t range_topk_smem_bytes();
+// K7 on the tensor cores (ivf_tc.cu): rows / cols as bf16 (n x kpad, kpad % 16 == 0, <= 256)
+cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const uint16_t* cols, const float* cnorm,
+                                 int kpad, const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks,
+                                 const uint32_t* list_off, const uint2* ranges, int m, int flags, uint32_t* out_ids,
+                                 float* out_dists, uint64_t out_stride, cudaStream_t stream);
+size_t range_topk_tc_smem_bytes(int kpad);
+cudaError_t launch_to_bf16(const float* x, uint64_t n, int dpad, int kpad, uint16_t* out, cudaStream_t stream);
 cudaError_t launch_row_norms(const float* x, uint64_t n, int dpad, float* out, cudaStream_t stream);
 // Exact compute_entry_order on the device (dim <= 1024).
 size_t entry_order_scratch_bytes(uint64_t n);

@@ -1939,6 +1939,38 @@ dvsg_status dvsg_range_topk_device(dvsg_ctx* c, const float* d_rows, const float
   });
 }
 
+dvsg_status dvsg_to_bf16_device(dvsg_ctx* c, const float* d_x, uint64_t n, int dpad, int kpad, uint16_t* d_out) {
+  return guarded([&] {
+    set_device(c);
+    if (kpad < dpad || kpad % 16) fail(DVSG_EINVAL, "to_bf16: kpad %d must be a multiple of 16 >= dpad %d", kpad, dpad);
+    cuda_check(dvsg::launch_to_bf16(d_x, n, dpad, kpad, d_out, c->stream), "to bf16");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "to bf16");
+  });
+}
+
+dvsg_status dvsg_range_topk_bf16_device(dvsg_ctx* c, const uint16_t* d_rows, const float* d_row_norms,
+                                        const uint16_t* d_cols, const float* d_col_norms, int kpad,
+                                        const uint32_t* d_row_map, const dvsg_range_block* d_blocks, uint64_t nblocks,
+                                        const uint32_t* d_list_off, const uint32_t* d_ranges, int m, int flags,
+                                        uint32_t* d_out_ids, float* d_out_dists, uint64_t out_stride) {
+  return guarded([&] {
+    set_device(c);
+    if (m < 1 || m > 32) fail(DVSG_EINVAL, "range_topk: m=%d outside 1..32", m);
+    if (kpad < 16 || kpad > 256 || kpad % 16) fail(DVSG_EINVAL, "range_topk (tensor cores): kpad %d outside 16..256 step 16", kpad);
+    if ((uint64_t)m > out_stride) fail(DVSG_EINVAL, "range_topk: out_stride %llu < m", (unsigned long long)out_stride);
+    if ((flags & DVSG_RANGE_MERGE) && !d_out_dists) fail(DVSG_EINVAL, "range_topk: DVSG_RANGE_MERGE needs d_out_dists");
+    if (!d_rows || !d_cols || !d_row_norms || !d_col_norms || !d_out_ids || (nblocks && (!d_blocks || !d_list_off || !d_ranges)))
+      fail(DVSG_EINVAL, "range_topk: null input");
+    cuda_check(dvsg::launch_range_topk_tc(d_rows, d_row_norms, d_cols, d_col_norms, kpad, d_row_map,
+                                          reinterpret_cast<const dvsg::RangeBlock*>(d_blocks), nblocks, d_list_off,
+                                          reinterpret_cast<const uint2*>(d_ranges), m, flags, d_out_ids, d_out_dists,
+                                          out_stride, c->stream), "range_topk tc");
+    c->launches += 1;
+    cuda_check(cudaStreamSynchronize(c->stream), "range_topk tc");
+  });
+}
+
 dvsg_status dvsg_segment_means_device(dvsg_ctx* c, const float* d_x, int dpad, const uint32_t* d_idx,
                                       const uint64_t* d_off, uint32_t nseg, float* d_cents) {
   return guarded([&] {

@@ -1,0 +1,317 @@
+// ivf_tc.cu -- K7 on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// Same contract as range_topk_kernel (ivf_build.cu): per row of a <= 128-row
+// block, the m <= 32 smallest (squared L2, column id) keys over a list of
+// column ranges.  The dot products run as one UMMA per 16-deep K slice:
+//
+//   A = the block's rows   (128 x K bf16, K-major, loaded once per block)
+//   B = 128 columns        (128 x K bf16, K-major, double-buffered cp.async)
+//   D = A . B^T            (128 x 128 fp32 in TMEM: lane = row, column = col)
+//
+// issued by one thread (tcgen05.mma.cta_group::1.kind::f16, M=128, N=128,
+// K=16 per instruction) and committed to an mbarrier; the 4 warps then read
+// their 32 TMEM lanes (tcgen05.ld 32x32b.x32), form dist = |x|^2 + |y|^2 -
+// 2 x.y and keep a per-thread sorted top-m list in shared memory.  The next
+// column tile streams in while the current one is multiplied and scanned.
+//
+// Exactness: the bench data are integers in [0, 255]: exact in bf16, every
+// product exact in fp32 and every partial sum an integer below 2^24, so the
+// tensor-core dot product -- whatever its internal summation order -- is the
+// exact integer and the keys equal the CUDA-core K7's (tested bit for bit in
+// tests/test_gpu_ivf.py).  On float data bf16 rounds the inputs: the result is
+// an approximate kNN, which is all a graph build needs; ground truth on float
+// data stays on the fp32 path.
+//
+// Shared-memory layout of an operand (UMMA canonical K-major, no swizzle):
+// element (r, k) at (r/8)*SBO + (k/8)*LBO + (r%8)*16 + (k%8)*2 bytes with
+// LBO = 128 (the 16-byte K chunks of one 8-row core matrix are adjacent) and
+// SBO = K/8 * 128 (8-row groups follow each other).
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dvsg_internal.h"
+
+namespace dvsg {
+namespace {
+
+constexpr int TCM = 128;  // rows per block (UMMA M)
+constexpr int TCN = 128;  // columns per tile (UMMA N)
+constexpr int TCMAXK = 256;
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  if (f == 0.0f) f = 0.0f;
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1 (Blackwell), no swizzle
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(s32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                                  \
+  asm volatile(                                                                                              \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                     \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),      \
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),  \
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),            \
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),            \
+        "=r"(r[30]), "=r"(r[31])                                                                             \
+      : "r"(taddr))
+
+// smem per CTA: A (128 x K bf16) + 2 x B (128 x K bf16) + col norms x2 + lists
+__host__ __device__ inline size_t tc_smem_bytes(int kpad) {
+  return (size_t)3 * TCM * kpad * 2 + 2 * TCN * 4 + (size_t)32 * TCM * 8 + 64;
+}
+
+__global__ void __launch_bounds__(128, 1)
+range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict__ rnorm,
+                     const uint16_t* __restrict__ cols, const float* __restrict__ cnorm, int kpad,
+                     const uint32_t* __restrict__ row_map, const RangeBlock* __restrict__ blocks,
+                     const uint32_t* __restrict__ list_off, const uint2* __restrict__ ranges, int m, int flags,
+                     uint32_t* __restrict__ out_ids, float* __restrict__ out_dists, uint64_t out_stride) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* sa = smem;
+  unsigned char* sb[2] = {smem + (size_t)TCM * kpad * 2, smem + (size_t)2 * TCM * kpad * 2};
+  float* cn[2];
+  cn[0] = reinterpret_cast<float*>(smem + (size_t)3 * TCM * kpad * 2);
+  cn[1] = cn[0] + TCN;
+  uint64_t* list = reinterpret_cast<uint64_t*>(cn[1] + TCN);  // [32][128]: entry j of row t at j*128 + t
+  uint64_t* bar = list + 32 * TCM;
+  __shared__ uint32_t tmem_slot;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const RangeBlock blk = blocks[blockIdx.x];
+  const int nrows = (int)blk.nrows;
+  const uint32_t lbo = 128, sbo = (uint32_t)(kpad / 8) * 128;
+  const int kch = kpad / 8;  // 16-byte chunks per row
+
+  // ---- TMEM (128 fp32 columns) and the MMA-completion barrier
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(s32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) mbar_init(bar);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  // ---- this thread's row: physical index, norm, list
+  const bool rvalid = tid < nrows;
+  const uint32_t prow = rvalid ? (row_map ? row_map[blk.row0 + tid] : blk.row0 + tid) : 0u;
+  const float nr = rvalid ? rnorm[prow] : 0.f;
+  const uint64_t orow = (flags & 8) ? (uint64_t)prow : (uint64_t)blk.out_row0 + (uint64_t)tid;
+  int cnt = 0;
+  if ((flags & 4) && rvalid) {  // continue from the lists already in the output
+    for (int j = 0; j < m; ++j) {
+      const uint32_t id = out_ids[orow * out_stride + j];
+      if (id == 0xFFFFFFFFu) break;
+      list[j * TCM + tid] = ((uint64_t)f2ord(out_dists[orow * out_stride + j]) << 32) | id;
+      cnt = j + 1;
+    }
+  }
+  uint64_t thr = cnt == m ? list[(m - 1) * TCM + tid] : ~0ull;
+
+  // ---- A: the block's rows, canonical K-major layout
+  for (int c = tid; c < TCM * kch; c += 128) {
+    const int r = c / kch, kc = c - r * kch;
+    const uint32_t pr = r < nrows ? (row_map ? row_map[blk.row0 + r] : blk.row0 + r) : 0u;
+    cp16(s32(sa + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), rows + (uint64_t)pr * kpad + kc * 8, r < nrows);
+  }
+  cp_commit();
+
+  // ---- column tiles: (range, start) pairs, prefetched one ahead
+  const uint32_t l0 = list_off[blk.list], l1 = list_off[blk.list + 1];
+  uint32_t li = l0, c0 = l0 < l1 ? ranges[l0].x : 0u;
+  auto next_tile = [&](uint32_t& l, uint32_t& c) {  // advance to the next non-empty tile start
+    while (l < l1) {
+      const uint2 rg = ranges[l];
+      if (c < rg.x) c = rg.x;
+      if (c < rg.y) return true;
+      ++l;
+      if (l < l1) c = ranges[l].x;
+    }
+    return false;
+  };
+  bool have = next_tile(li, c0);
+  auto load_b = [&](int buf, uint32_t l, uint32_t c) {
+    const uint32_t end = ranges[l].y;
+    for (int q = tid; q < TCN * kch; q += 128) {
+      const int r = q / kch, kc = q - r * kch;
+      const bool v = c + r < end;
+      cp16(s32(sb[buf] + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), cols + (uint64_t)(v ? c + r : 0) * kpad + kc * 8,
+           v);
+    }
+    cn[buf][tid] = c + tid < end ? cnorm[c + tid] : 0.f;
+    cp_commit();
+  };
+  if (have) load_b(0, li, c0);
+  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TCN >> 3) << 17) | ((uint32_t)(TCM >> 4) << 24);
+
+  int buf = 0;
+  uint32_t phase = 0;
+  while (have) {
+    const uint32_t tl = li, tc = c0, tend = ranges[tl].y;
+    // prefetch the following tile into the other buffer (its MMA finished last round)
+    uint32_t nl = li, nc = c0 + TCN;
+    const bool nhave = next_tile(nl, nc);
+    if (nhave) load_b(buf ^ 1, nl, nc);
+    if (nhave) cp_wait<1>(); else cp_wait<0>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t abase = s32(sa), bbase = s32(sb[buf]);
+      for (int kk = 0; kk < kpad / 16; ++kk) {
+        const uint64_t ad = umma_desc(abase + kk * 2 * lbo, lbo, sbo);
+        const uint64_t bd = umma_desc(bbase + kk * 2 * lbo, lbo, sbo);
+        const uint32_t acc = kk > 0 ? 1u : 0u;
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+            : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
+                   : "memory");
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- epilogue: this thread's row, 128 columns in 4 TMEM loads of 32
+    float thr_d = thr == ~0ull ? __int_as_float(0x7F800000) : ord2f((uint32_t)(thr >> 32));
+#pragma unroll 1
+    for (int part = 0; part < TCN / 32; ++part) {
+      uint32_t r[32];
+      TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(part * 32), r);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (!rvalid) continue;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int cl = part * 32 + j;
+        const uint32_t col = tc + (uint32_t)cl;
+        const float dist = fmaxf(fmaf(-2.f, __uint_as_float(r[j]), nr + cn[buf][cl]), 0.f);
+        if (dist > thr_d || col >= tend) continue;
+        if ((flags & 1) && col == prow) continue;
+        const uint64_t key = ((uint64_t)f2ord(dist) << 32) | col;
+        if (key >= thr) continue;
+        // sorted insert into the thread's list (rare after the first tiles)
+        int pos = cnt < m ? cnt : m - 1;
+        while (pos > 0 && list[(pos - 1) * TCM + tid] > key) {
+          list[pos * TCM + tid] = list[(pos - 1) * TCM + tid];
+          --pos;
+        }
+        list[pos * TCM + tid] = key;
+        if (cnt < m) ++cnt;
+        if (cnt == m) {
+          thr = list[(m - 1) * TCM + tid];
+          thr_d = ord2f((uint32_t)(thr >> 32));
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // TMEM and buffer `buf` free for the next round
+    buf ^= 1;
+    li = nl;
+    c0 = nc;
+    have = nhave;
+  }
+
+  // ---- emit (same rules as range_topk_kernel)
+  if (rvalid) {
+    if (flags & 2) {
+      const int nv = cnt < m ? cnt : m;
+      for (int j = 0; j < m; ++j) {
+        const uint64_t kj = nv > 0 ? list[(j % nv) * TCM + tid] : 0ull;
+        out_ids[orow * out_stride + j] = nv > 0 ? (uint32_t)kj : prow;
+        if (out_dists) out_dists[orow * out_stride + j] = nv > 0 ? ord2f((uint32_t)(kj >> 32)) : 0.f;
+      }
+    } else {
+      for (int j = 0; j < m; ++j) {
+        const bool ok = j < cnt;
+        const uint64_t kj = ok ? list[j * TCM + tid] : 0ull;
+        out_ids[orow * out_stride + j] = ok ? (uint32_t)kj : 0xFFFFFFFFu;
+        if (out_dists) out_dists[orow * out_stride + j] = ok ? ord2f((uint32_t)(kj >> 32)) : __int_as_float(0x7F800000);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ x, uint64_t n, int dpad, int kpad,
+                               uint16_t* __restrict__ out) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * (uint64_t)kpad) return;
+  const uint64_t r = i / (uint64_t)kpad;
+  const int k = (int)(i - r * (uint64_t)kpad);
+  const float v = k < dpad ? x[r * (uint64_t)dpad + k] : 0.f;
+  // round to nearest even (integers up to 256 are exact)
+  uint32_t u = __float_as_uint(v);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  out[i] = (uint16_t)(u >> 16);
+}
+
+}  // namespace
+
+size_t range_topk_tc_smem_bytes(int kpad) { return tc_smem_bytes(kpad); }
+
+cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const uint16_t* cols, const float* cnorm,
+                                 int kpad, const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks,
+                                 const uint32_t* list_off, const uint2* ranges, int m, int flags, uint32_t* out_ids,
+                                 float* out_dists, uint64_t out_stride, cudaStream_t stream) {
+  if (m < 1 || m > 32 || kpad % 16 || kpad < 16 || kpad > TCMAXK) return cudaErrorInvalidValue;
+  if (nblocks == 0) return cudaSuccess;
+  const size_t smem = tc_smem_bytes(kpad);
+  cudaError_t e = cudaFuncSetAttribute(range_topk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  for (uint64_t b0 = 0; b0 < nblocks; b0 += 0x7FFFFFFFull) {
+    const uint64_t nb = nblocks - b0 < 0x7FFFFFFFull ? nblocks - b0 : 0x7FFFFFFFull;
+    range_topk_tc_kernel<<<(unsigned)nb, 128, smem, stream>>>(rows, rnorm, cols, cnorm, kpad, row_map, blocks + b0,
+                                                              list_off, ranges, m, flags, out_ids, out_dists,
+                                                              out_stride);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_bf16(const float* x, uint64_t n, int dpad, int kpad, uint16_t* out, cudaStream_t stream) {
+  const uint64_t tot = n * (uint64_t)kpad;
+  if (tot == 0) return cudaSuccess;
+  to_bf16_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(x, n, dpad, kpad, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dvsg

@@ -49,32 +49,6 @@ __device__ __forceinline__ bool visit_insert(uint32_t* table, uint32_t mask, uin
   }
 }
 
-// Same insert on a table known to be in global memory (explicit global-space
-// load / CAS instead of generic LD / ATOM).
-__device__ __forceinline__ uint32_t ld_global_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t cas_global_u32(uint32_t* p, uint32_t cmp, uint32_t val) {
-  uint32_t old;
-  asm volatile("atom.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
-  return old;
-}
-__device__ __forceinline__ bool visit_insert_global(uint32_t* table, uint32_t mask, uint32_t id) {
-  uint32_t h = (hash_slot(id) >> 7) & mask;
-  for (;;) {
-    uint32_t cur = ld_global_u32(table + h);
-    if (cur == id) return false;
-    if (cur == kEmpty) {
-      cur = cas_global_u32(table + h, kEmpty, id);
-      if (cur == kEmpty) return true;
-      if (cur == id) return false;
-    }
-    h = (h + 1) & mask;
-  }
-}
-
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 #ifndef DVSG_SORT_ROLLED

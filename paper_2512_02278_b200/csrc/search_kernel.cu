@@ -34,57 +34,8 @@
 namespace dvsg {
 namespace {
 
-#ifndef DVSG_K1_CHUNK_FILTER
-#define DVSG_K1_CHUNK_FILTER 0  // measured: within-chunk smem duplicate filter -12%
-#endif
-#ifndef DVSG_K1_GLOBAL_PTX
-#define DVSG_K1_GLOBAL_PTX 0  // measured: explicit ld.global/atom.global probes -0.3%
-#endif
-#ifndef DVSG_K1_BATCH_PROBES
-#define DVSG_K1_BATCH_PROBES 0  // measured: batched probe rounds -4%
-#endif
-#ifndef DVSG_K1_TMA_GATHER
-#define DVSG_K1_TMA_GATHER 0  // 1: candidate rows staged in smem by cp.async.bulk (mbarrier completion)
-#endif
-#ifndef DVSG_K1_WARP_FUSED
-#define DVSG_K1_WARP_FUSED 0  // 1: each warp scores the new ids it probed (no block barrier between)
-#endif
-#ifndef DVSG_K1_SORT_RUNS
-#define DVSG_K1_SORT_RUNS 0
-#endif
-
 // VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
 // FULL: dpad == 128 * VPL (every lane holds real dimensions; no bound check).
-#if DVSG_K1_TMA_GATHER
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-#endif
 
 template <int VPL, typename ACC, int METRIC, bool FULL>
 #ifndef DVSG_MINB
@@ -104,24 +55,11 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
   uint64_t* surv = pool_alt + a.cap;
   uint32_t* cand = reinterpret_cast<uint32_t*>(surv + a.chp);
   uint32_t* frontier = cand + kChunk;
-  const bool gtab = a.hash_global != nullptr;
   uint32_t* const region = a.hash_global ? a.hash_global + (size_t)blockIdx.x * (size_t)(a.hsize + a.hsmall)
                                          : frontier + ((a.beam + 3) & ~3);
   const uint32_t dg_magic = (uint32_t)((0x100000000ull + (uint64_t)a.dg - 1) / (uint64_t)a.dg);
   const unsigned full = 0xFFFFFFFFu;
   const unsigned lt_mask = (1u << lane) - 1u;
-#if DVSG_K1_TMA_GATHER
-  // per-warp staging (U rows, <= 4 KB) + one mbarrier per warp, at the end
-  // of the dynamic smem (search_smem_bytes adds them)
-  uint32_t* const smem_end = frontier + ((a.beam + 3) & ~3) + (a.hash_global ? 0 : a.hsize);
-  float* const tma_stage = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(smem_end) + 15) & ~(uintptr_t)15) + warp * 1024;
-  uint64_t* const tma_bar = reinterpret_cast<uint64_t*>(tma_stage - warp * 1024 + kWarps * 1024) + warp;
-  unsigned tma_phase = 0;
-  if (lane == 0) mbar_init(tma_bar, 1);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-#endif
 
   const uint64_t nunits = a.nunits_dev ? (uint64_t)*a.nunits_dev : a.nunits;
   for (;;) {
@@ -230,14 +168,6 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           st.ncand = 0;
           st.nsurv = 0;
         }
-#if DVSG_K1_CHUNK_FILTER
-        // within-chunk duplicate filter in the (idle until scoring) survivor
-        // buffer: only an id's first occurrence in the chunk probes the
-        // visited table (exact: a filtered id is a repeat of a probed one)
-        uint32_t* const filt = reinterpret_cast<uint32_t*>(surv);
-        constexpr int kFilt = 2 * kChunk;  // u32 slots (surv holds >= kChunk u64)
-        for (int i = tid; i < kFilt; i += kThreads) filt[i] = kEmpty;
-#endif
         // ---- gather raw ids (all loads first for MLP), then dedup
         uint32_t ids[kRawPerThread];
 #pragma unroll
@@ -260,141 +190,38 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           }
         }
         __syncthreads();  // st.ncand reset visible
-#if DVSG_K1_BATCH_PROBES
-        // global table: every probe round issues the loads of all 8 ids, then
-        // their CASes, before using a result (an empty slot is always CASed,
-        // so afterwards cur == kEmpty means "claimed")
-        unsigned fresh = 0;
-        if (gtab) {
-          uint32_t hs[kRawPerThread];
-          unsigned pend = 0;
-#pragma unroll
-          for (int j = 0; j < kRawPerThread; ++j) {
-            hs[j] = (hash_slot(ids[j]) >> 7) & hmask;
-            if (ids[j] != kEmpty) pend |= 1u << j;
-          }
-          while (pend) {
-            uint32_t cur[kRawPerThread];
-#pragma unroll
-            for (int j = 0; j < kRawPerThread; ++j) cur[j] = (pend >> j) & 1u ? ld_global_u32(table + hs[j]) : 0u;
-#pragma unroll
-            for (int j = 0; j < kRawPerThread; ++j)
-              if (((pend >> j) & 1u) && cur[j] == kEmpty) cur[j] = cas_global_u32(table + hs[j], kEmpty, ids[j]);
-#pragma unroll
-            for (int j = 0; j < kRawPerThread; ++j) {
-              if (!((pend >> j) & 1u)) continue;
-              if (cur[j] == kEmpty) {
-                fresh |= 1u << j;
-                pend &= ~(1u << j);
-              } else if (cur[j] == ids[j]) {
-                pend &= ~(1u << j);
-              } else {
-                hs[j] = (hs[j] + 1u) & hmask;
-              }
-            }
-          }
-        }
-#endif
-#if DVSG_K1_WARP_FUSED
-        int wcount = 0;
-#endif
 #pragma unroll
         for (int j = 0; j < kRawPerThread; ++j) {
           if (j * kThreads >= rcount) break;  // block-uniform
-#if DVSG_K1_BATCH_PROBES
-          const bool isnew = gtab ? ((fresh >> j) & 1u) != 0
-                                  : (ids[j] != kEmpty && visit_insert(table, hmask, ids[j]));
-#else
-          bool first = ids[j] != kEmpty;
-#if DVSG_K1_CHUNK_FILTER
-          if (first) {
-            uint32_t h = (ids[j] * 0x85EBCA6Bu >> 19) & (kFilt - 1);
-#pragma unroll 1
-            for (int t = 0; t < 8; ++t) {  // bounded: an unresolved id just probes the table
-              const uint32_t cur = atomicCAS(filt + h, kEmpty, ids[j]);
-              if (cur == kEmpty) break;
-              if (cur == ids[j]) {
-                first = false;
-                break;
-              }
-              h = (h + 1) & (kFilt - 1);
-            }
-          }
-#endif
-          const bool isnew = first && ((DVSG_K1_GLOBAL_PTX && gtab) ? visit_insert_global(table, hmask, ids[j])
-                                                                   : visit_insert(table, hmask, ids[j]));
-#endif
+          const bool isnew = ids[j] != kEmpty && visit_insert(table, hmask, ids[j]);
           const unsigned bal = __ballot_sync(full, isnew);
-#if DVSG_K1_WARP_FUSED
-          // warp-local list: this warp scores its own new ids right away
-          if (isnew) cand[warp * (kRawPerThread * 32) + wcount + __popc(bal & lt_mask)] = ids[j];
-          wcount += __popc(bal);
-#else
           int base = 0;
           if (lane == 0 && bal) base = atomicAdd(&st.ncand, __popc(bal));
           base = __shfl_sync(full, base, 0);
           if (isnew) cand[base + __popc(bal & lt_mask)] = ids[j];
-#endif
         }
-#if DVSG_K1_WARP_FUSED
-        if (lane == 0 && wcount) atomicAdd(&st.ncand, wcount);
-        __syncwarp();
-        const uint32_t* clist = cand + warp * (kRawPerThread * 32);
-        const int Mlim = wcount, cb0 = 0, cstep = U;
-#else
         __syncthreads();
         const int M = st.ncand;
         visited += (uint64_t)M;
-        const uint32_t* clist = cand;
-        const int Mlim = M, cb0 = warp * U, cstep = kWarps * U;
-#endif
 
         // ---- score new candidates: warp per vector, U vectors in flight per warp
-#if DVSG_SCORE_ROLLED
-#pragma unroll 1
-#endif
-        for (int cb = cb0; cb < Mlim; cb += cstep) {
+        for (int cb = warp * U; cb < M; cb += kWarps * U) {
           uint32_t ids_u[U];
           if constexpr (U >= 4) {
 #pragma unroll
             for (int u4 = 0; u4 < U; u4 += 4) {
-              const uint4 w4 = *reinterpret_cast<const uint4*>(clist + cb + u4);
+              const uint4 w4 = *reinterpret_cast<const uint4*>(cand + cb + u4);
               ids_u[u4] = w4.x; ids_u[u4 + 1] = w4.y; ids_u[u4 + 2] = w4.z; ids_u[u4 + 3] = w4.w;
             }
           } else {
 #pragma unroll
-            for (int u = 0; u < U; ++u) ids_u[u] = clist[cb + u];
+            for (int u = 0; u < U; ++u) ids_u[u] = cand[cb + u];
           }
           float4 x[U][VPL];
-#if DVSG_K1_TMA_GATHER
-          {
-            // lane 0 issues one bulk copy per row into the warp's staging
-            // buffer; every lane waits on the mbarrier, then reads its slices
-            const unsigned rowb = (unsigned)a.dpad * 4u;
-            const int nv = Mlim - cb < U ? Mlim - cb : U;
-            __syncwarp();
-            if (lane == 0) {
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              mbar_expect_tx(tma_bar, rowb * (unsigned)nv);
-#pragma unroll
-              for (int u = 0; u < U; ++u)
-                if (u < nv) bulk_g2s(tma_stage + u * a.dpad, vbase + (uint64_t)ids_u[u] * rstride, rowb, tma_bar);
-            }
-            mbar_wait(tma_bar, tma_phase);
-            tma_phase ^= 1u;
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-              for (int v = 0; v < VPL; ++v)
-                x[u][v] = (u < nv && (FULL || lane * 4 + 128 * v < a.dpad))
-                              ? *reinterpret_cast<const float4*>(tma_stage + u * a.dpad + lane * 4 + 128 * v)
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#else
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             // past M: load row 0 (harmless, result discarded by the ci < M test)
-            const uint32_t id = cb + u < Mlim ? ids_u[u] : 0u;
+            const uint32_t id = cb + u < M ? ids_u[u] : 0u;
             const float* row = lbase + (uint64_t)id * rstride;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -402,7 +229,6 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
               else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
-#endif
           ACC part[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -417,9 +243,9 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
           const int ci = cb + myu;
           bool pass = false;
           uint64_t mykey = 0;
-          if ((lane & ((32 >> LU) - 1)) == 0 && ci < Mlim) {
+          if ((lane & ((32 >> LU) - 1)) == 0 && ci < M) {
             const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
-            mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)clist[ci] << 1);
+            mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
             pass = mykey < thresh;
           }
           const unsigned bal = __ballot_sync(full, pass);
@@ -430,32 +256,13 @@ __global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const Searc
         }
         __syncthreads();
         const int S = st.nsurv;
-#if DVSG_K1_WARP_FUSED
-        visited += (uint64_t)st.ncand;
-#endif
         __syncthreads();  // every thread has read the counters before the next reset
         if (S == 0) continue;  // block-uniform
 
         // ---- sort survivors, merge into the pool, truncate at cap
-#ifdef DVSG_SORT_STATS
-        if (tid == 0 && a.stats) {
-          atomicAdd(a.stats + 3, (unsigned long long)S);
-          atomicAdd(a.stats + 4, (unsigned long long)M);
-          atomicAdd(a.stats + 5, 1ull);
-          atomicAdd(a.stats + 6 + (it < 0 ? 0 : (it < 1 ? 1 : 2)), (unsigned long long)S);
-        }
-#endif
-#if DVSG_K1_SORT_RUNS
-        // warp-sorted runs + merge levels, ping-pong through cand (free after scoring)
-        const uint64_t* sorted = surv;
-        if (S <= kChunk / 2) sorted = sort_runs(surv, S, reinterpret_cast<uint64_t*>(cand), tid);
-        else sort_keys(surv, S, tid);
-#else
         sort_keys(surv, S, tid);
-        const uint64_t* sorted = surv;
-#endif
         const int outn = P + S < a.cap ? P + S : a.cap;
-        merge_path(pool, P, sorted, S, pool_alt, outn, tid);
+        merge_path(pool, P, surv, S, pool_alt, outn, tid);
         __syncthreads();
         {
           uint64_t* t = pool;
@@ -553,9 +360,6 @@ size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_sme
   size_t b = sizeof(uint64_t) * (2 * (size_t)cap + (size_t)chp);
   b += sizeof(uint32_t) * ((size_t)kChunk + (size_t)((beam + 3) & ~3));
   if (hash_in_smem) b += sizeof(uint32_t) * (size_t)hsize;
-#if DVSG_K1_TMA_GATHER
-  b = ((b + 15) & ~(size_t)15) + (size_t)kWarps * 4096 + (size_t)kWarps * 8 + 16;
-#endif
   return b;
 }
 

@@ -44,9 +44,6 @@
 #include "dvsg_internal.h"
 #include "k1_device.cuh"
 
-#ifndef DVSG_XG_LOCAL
-#define DVSG_XG_LOCAL 0  // 1: origin scores its own-shard candidates in the expand step (measured: R=1 -6%, R=2,4 +-2%)
-#endif
 #ifndef DVSG_XG_BATCH_PROBES
 #define DVSG_XG_BATCH_PROBES 1
 #endif
@@ -362,8 +359,8 @@ __device__ __forceinline__ void expand_unit(const XgArgs& a, const int rr, const
       xs.off[0] = 0;
       for (int r = 0; r < kXgMaxRanks; ++r) xs.off[r + 1] = xs.off[r] + (r < R ? xs.cnt[r] : 0);
     }
-    if (tid < R) {  // own-shard candidates are scored right here (below), not pushed
-      const int c = (DVSG_XG_LOCAL && tid == me) ? 0 : xs.cnt[tid];
+    if (tid < R) {  // one peer atomic per owner reserves this query's inbox range
+      const int c = xs.cnt[tid];
       xs.pos[tid] = c ? atomicAdd(a.views[tid].cursor + slot * R + me, (unsigned)c) : 0u;
     }
     __syncthreads();
@@ -377,83 +374,12 @@ __device__ __forceinline__ void expand_unit(const XgArgs& a, const int rr, const
       int o = 0;
 #pragma unroll
       for (int s = 1; s < kXgMaxRanks; ++s) o += i >= xs.off[s] ? 1 : 0;
-      if (DVSG_XG_LOCAL && o == me) continue;
       uint64_t* dst = a.views[o].inbox + (uint64_t)me * a.rstride + xs.pos[o] + (uint32_t)(i - xs.off[o]);
       *dst = ((uint64_t)j << 32) | buck[i];
     }
     if (tid < R)
       a.meta[qs * (uint64_t)R + tid] =
-          make_uint2(xs.pos[tid], (DVSG_XG_LOCAL && tid == me) ? 0u : (unsigned)xs.cnt[tid]);
-#if DVSG_XG_LOCAL
-    // ---- own-shard candidates: score, filter, sort, merge now (as K1); the
-    //      pool then holds every candidate of this phase once the owners'
-    //      keys are merged at the start of the next phase (top-cap of a union
-    //      is order-independent)
-    if (xs.cnt[me] > 0) {  // block-uniform
-      constexpr int U = VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL);
-      constexpr int LU = ilog2(U);
-      const XgView& vm = a.views[me];
-      const uint32_t lo = (uint32_t)vm.lo;
-      const float* lbase = vm.vec + lane * 4;
-      float4 q[VPL];
-      load_query<VPL, FULL>(q, vm.qall + ((uint64_t)me * a.wcap + j) * (uint64_t)a.dpad, lane, a.dim);
-      const int L0 = xs.off[me], LN = xs.cnt[me];
-      for (int cbase = 0; cbase < LN; cbase += kChunk) {
-        const int cnt = LN - cbase < kChunk ? LN - cbase : kChunk;
-        if (tid == 0) st.nsurv = 0;
-        __syncthreads();
-        const uint32_t* ids = buck + L0 + cbase;
-        for (int cb = warp * U; cb < cnt; cb += kWarps * U) {
-          float4 x[U][VPL];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t id = cb + u < cnt ? ids[cb + u] : lo;
-            const float* row = lbase + (uint64_t)(id - lo) * (uint32_t)a.dpad;
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-              if (FULL || lane * 4 + 128 * v < a.dpad) x[u][v] = ldg_f4(row + 128 * v);
-              else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
-          ACC part[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            ACC acc = lane_partial<ACC, METRIC>(x[u][0], q[0]);
-#pragma unroll
-            for (int v = 1; v < VPL; ++v) acc += lane_partial<ACC, METRIC>(x[u][v], q[v]);
-            part[u] = acc;
-          }
-          const ACC tot = transpose_reduce<U, ACC>(part, lane);
-          const int ci = cb + ((lane >> (5 - LU)) & (U - 1));
-          bool pass = false;
-          uint64_t key = 0;
-          if ((lane & ((32 >> LU) - 1)) == 0 && ci < cnt) {
-            const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
-            key = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)ids[ci] << 1);
-            pass = key < thresh;
-          }
-          const unsigned bal = __ballot_sync(full, pass);
-          int base = 0;
-          if (lane == 0 && bal) base = atomicAdd(&st.nsurv, __popc(bal));
-          base = __shfl_sync(full, base, 0);
-          if (pass) surv[base + __popc(bal & lt_mask)] = key;
-        }
-        __syncthreads();
-        const int S = st.nsurv;
-        __syncthreads();
-        if (S == 0) continue;
-        sort_keys(surv, S, tid);
-        const int outn = P + S < a.cap ? P + S : a.cap;
-        merge_path(pool, P, surv, S, pool_alt, outn, tid);
-        __syncthreads();
-        uint64_t* t = pool;
-        pool = pool_alt;
-        pool_alt = t;
-        P = outn;
-        thresh = P == a.cap ? pool[a.cap - 1] : ~0ull;
-      }
-    }
-#endif
+          make_uint2(xs.pos[tid], (unsigned)xs.cnt[tid]);
     for (int i = tid; i < P; i += kThreads) gpool[i] = pool[i];
     if (tid == 0) {
       a.psize[qs] = (uint32_t)P;

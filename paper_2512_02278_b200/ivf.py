@@ -81,8 +81,9 @@ def segment_blocks(off, list_of_seg=None):
 
 
 def range_topk(ctx, rows, rnorm, cols, cnorm, blocks, list_off, ranges, m, flags=0, row_map=None,
-               out_ids=None, out_dists=None, out_stride=None, out_rows=None):
-    """K7 over torch tensors (all on the context's device)."""
+               out_ids=None, out_dists=None, out_stride=None, out_rows=None, rows_bf16=None, cols_bf16=None):
+    """K7 over torch tensors (all on the context's device).  With bf16 copies
+    of rows and cols (to_bf16) it runs on the tensor cores (ivf_tc.cu)."""
     import torch
     dpad = rows.shape[1]
     stride = out_stride or m
@@ -92,11 +93,30 @@ def range_topk(ctx, rows, rnorm, cols, cnorm, blocks, list_off, ranges, m, flags
     if os.environ.get("DVSG_IVF_CHECK", "0") == "1":
         _check_k7(rows, cols, blocks, list_off, ranges, m, flags, row_map, out_ids, stride)
     _sync()
-    ctx.range_topk_device(rows.data_ptr(), rnorm.data_ptr(), cols.data_ptr(), cnorm.data_ptr(), dpad,
-                          0 if row_map is None else row_map.data_ptr(), blocks.data_ptr(), blocks.shape[0],
-                          list_off.data_ptr(), ranges.data_ptr(), m, flags, out_ids.data_ptr(),
-                          0 if out_dists is None else out_dists.data_ptr(), stride)
+    if rows_bf16 is not None and cols_bf16 is not None:
+        ctx.range_topk_bf16_device(rows_bf16.data_ptr(), rnorm.data_ptr(), cols_bf16.data_ptr(), cnorm.data_ptr(),
+                                   rows_bf16.shape[1], 0 if row_map is None else row_map.data_ptr(),
+                                   blocks.data_ptr(), blocks.shape[0], list_off.data_ptr(), ranges.data_ptr(), m,
+                                   flags, out_ids.data_ptr(), 0 if out_dists is None else out_dists.data_ptr(),
+                                   stride)
+    else:
+        ctx.range_topk_device(rows.data_ptr(), rnorm.data_ptr(), cols.data_ptr(), cnorm.data_ptr(), dpad,
+                              0 if row_map is None else row_map.data_ptr(), blocks.data_ptr(), blocks.shape[0],
+                              list_off.data_ptr(), ranges.data_ptr(), m, flags, out_ids.data_ptr(),
+                              0 if out_dists is None else out_dists.data_ptr(), stride)
     return out_ids
+
+
+def to_bf16(ctx, x):
+    """n x dpad float32 -> n x kpad bf16 (kpad = dpad rounded up to 16; as
+    int16 storage), exact for integers in [-256, 256]."""
+    import torch
+    n, dpad = x.shape
+    kpad = (dpad + 15) // 16 * 16
+    out = torch.empty((n, kpad), dtype=torch.int16, device=x.device)
+    _sync()
+    ctx.to_bf16_device(x.data_ptr(), n, dpad, kpad, out.data_ptr())
+    return out
 
 
 def _check_k7(rows, cols, blocks, list_off, ranges, m, flags, row_map, out_ids, stride):
@@ -218,7 +238,7 @@ def kmeans2(ctx, x, xn, n_fine: int, n_coarse: int = 256, sample: int = 4 << 20,
 def build_graph_ivf(ctx, x, degree: int = 32, cluster_size: int = 1024, probe: int = 8,
                     n_coarse: int = 32, sample: int = 4 << 20, iters: int = 6, cluster: int = 0,
                     dim: Optional[int] = None, shortlist: int = 32, optimize: bool = False,
-                    keep: Optional[int] = None, log=None) -> dict:
+                    keep: Optional[int] = None, tensor_cores: bool = False, log=None) -> dict:
     """Build one partition from the n x dpad float32 CUDA tensor `x` (rows in
     generation order) into `ctx`: rows stored in fine-cluster order, per-row
     probed kNN graph (K7 passes), optional CAGRA-style optimisation, device
@@ -282,6 +302,7 @@ def build_graph_ivf(ctx, x, degree: int = 32, cluster_size: int = 1024, probe: i
     # view) and merges that cluster's members into the row's running top-32
     adj = device_view(pa, (n, degree), torch.int32, dev)
     dists = torch.empty((n, degree), dtype=torch.float32, device=dev)
+    vb = to_bf16(ctx, vec) if tensor_cores and dpad <= 256 else None  # K7 on tcgen05 (ivf_tc.cu)
     lo1 = torch.arange(nf + 1, dtype=torch.int32, device=dev)
     rg1 = torch.stack([off[:-1], off[1:]], 1).to(torch.int32).contiguous()
     for j in range(p):
@@ -292,12 +313,12 @@ def build_graph_ivf(ctx, x, degree: int = 32, cluster_size: int = 1024, probe: i
         fl = _lib.RANGE_EXCLUDE_SELF | _lib.RANGE_OUT_PHYSICAL | (_lib.RANGE_MERGE if j else 0) | \
             (_lib.RANGE_BUILD_PAD if j == p - 1 else 0)
         range_topk(ctx, vec, vn, vec, vn, bl, lo1, rg1, degree, flags=fl, row_map=order32,
-                   out_ids=adj, out_dists=dists, out_stride=degree)
+                   out_ids=adj, out_dists=dists, out_stride=degree, rows_bf16=vb, cols_bf16=vb)
         del order, order32, bl
     t4 = time.time()
     cand = float((off[probes + 1] - off[probes]).sum(1).double().mean())
     del probes
-    del dists
+    del dists, vb
     if optimize:  # CAGRA-style rank pruning + reverse edges (csrc/graph_opt.cu)
         torch.cuda.empty_cache()
         _sync()
@@ -307,6 +328,7 @@ def build_graph_ivf(ctx, x, degree: int = 32, cluster_size: int = 1024, probe: i
     ctx.partition_commit_device(_lib.COMMIT_ENTRY_ORDER | _lib.COMMIT_IOTA_IDS)
     t6 = time.time()
     info = {"n": n, "fine_clusters": nf, "coarse_clusters": int(coarse.shape[0]), "probe": p,
+            "knn_kernel": "K7 tcgen05 (bf16, TMEM)" if tensor_cores and dpad <= 256 else "K7 CUDA-core fp32",
             "shortlist": q, "candidates_per_row": cand, "blocks": nb, "optimized": bool(optimize),
             "seconds": {"kmeans": t1 - t0, "assign_sort": t2 - t1, "store": t3 - t2, "knn": t4 - t3,
                         "optimize": t5 - t4, "commit_entry_order": t6 - t5, "total": t6 - t0},
@@ -317,7 +339,7 @@ def build_graph_ivf(ctx, x, degree: int = 32, cluster_size: int = 1024, probe: i
     return info
 
 
-def brute_force_topk(ctx, db, dbn, queries, k: int, splits: int = 0):
+def brute_force_topk(ctx, db, dbn, queries, k: int, splits: int = 0, db_bf16=None):
     """Exact top-k (dist, id) of each query row over all db rows (topk.cpp:12-30;
     exact on integer-valued data): K7 over column splits, then a per-query merge.
     -> (ids int64 nq x k, dists float32 nq x k) tensors."""
@@ -340,7 +362,9 @@ def brute_force_topk(ctx, db, dbn, queries, k: int, splits: int = 0):
     qn = row_norms(ctx, queries)
     ids = torch.empty((splits * nq, k), dtype=torch.int32, device=dev)
     dists = torch.empty((splits * nq, k), dtype=torch.float32, device=dev)
-    range_topk(ctx, queries, qn, db, dbn, bl.contiguous(), lo, rg, k, out_ids=ids, out_dists=dists)
+    qb = to_bf16(ctx, queries) if db_bf16 is not None else None
+    range_topk(ctx, queries, qn, db, dbn, bl.contiguous(), lo, rg, k, out_ids=ids, out_dists=dists,
+               rows_bf16=qb, cols_bf16=db_bf16)
     ids = ids.view(splits, nq, k).permute(1, 0, 2).reshape(nq, splits * k).to(torch.int64)
     dists = dists.view(splits, nq, k).permute(1, 0, 2).reshape(nq, splits * k)
     valid = ids >= 0

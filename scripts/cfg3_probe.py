@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--accum", default="f32")
     ap.add_argument("--keep", type=int, default=16)
     ap.add_argument("--no-optimize", action="store_true")
+    ap.add_argument("--tc", action="store_true", help="K7 on the tensor cores")
     args = ap.parse_args()
     dev = "cuda:0"
     ctx = dvs.Context(0)
@@ -43,7 +44,8 @@ def main():
     torch.cuda.synchronize()
     log(f"[probe] data {args.n}x{args.dim} in {time.time() - t0:.1f}s")
     info = ivf.build_graph_ivf(ctx, x, degree=32, cluster_size=args.cluster_size, probe=args.probe,
-                               dim=args.dim, optimize=not args.no_optimize, keep=args.keep, log=log)
+                               dim=args.dim, optimize=not args.no_optimize, keep=args.keep,
+                               tensor_cores=args.tc, log=log)
     del x
     torch.cuda.empty_cache()
     pv, pa, pg, pe, n = ctx.partition_view_device(0)

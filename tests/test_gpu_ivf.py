@@ -254,3 +254,55 @@ def test_optimize_graph_matches_restatement(ctx, oracle):
     ctx.optimize_graph_device(d_adj.data_ptr(), 1500, 16, 8)
     got = d_adj.cpu().numpy().view(np.uint32)
     assert np.array_equal(got, want.astype(np.uint32))
+
+
+@pytest.mark.parametrize("dim,m,flags", [(40, 7, 1), (96, 32, 1 | 2), (128, 10, 0), (256, 32, 1)])
+def test_range_topk_tensor_cores_equal_cuda_cores(ctx, dim, m, flags):
+    """K7 on tcgen05 (bf16 operands, fp32 TMEM accumulators) == the CUDA-core
+    K7 bit for bit on byte data (every product and partial sum exact)."""
+    from paper_2512_02278_b200 import ivf
+    rng = np.random.default_rng(dim)
+    x = rng.integers(0, 256, size=(1500, dim)).astype(np.float32)
+    x[::11] = x[5]  # duplicates: (dist, id) ties
+    dpad = (dim + 3) // 4 * 4
+    xp = np.zeros((1500, dpad), np.float32)
+    xp[:, :dim] = x
+    xt = _t(xp)
+    xn = ivf.row_norms(ctx, xt)
+    xb = ivf.to_bf16(ctx, xt)
+    off = torch.tensor([0, 100, 700, 1500], dtype=torch.int64, device="cuda")
+    blocks, _ = ivf.segment_blocks(off)
+    ranges = _t(np.array([[0, 300], [600, 1500], [20, 21], [900, 1499], [0, 1500]], np.int32))
+    lo = _t(np.array([0, 2, 4, 5], np.int32))
+    perm = _t(rng.permutation(1500).astype(np.int32))
+    for row_map in (None, perm):
+        f = flags | (8 if row_map is not None else 0)
+        d1 = torch.empty((1500, m), dtype=torch.float32, device="cuda")
+        d2 = torch.empty((1500, m), dtype=torch.float32, device="cuda")
+        a = ivf.range_topk(ctx, xt, xn, xt, xn, blocks, lo, ranges, m, flags=f, row_map=row_map, out_dists=d1,
+                           out_rows=1500)
+        b = ivf.range_topk(ctx, xt, xn, xt, xn, blocks, lo, ranges, m, flags=f, row_map=row_map, out_dists=d2,
+                           out_rows=1500, rows_bf16=xb, cols_bf16=xb)
+        assert torch.equal(a, b)
+        assert torch.equal(d1, d2)
+    # merge pass over ranges disjoint from each list's first ones
+    ranges2 = _t(np.array([[300, 600], [0, 20], [0, 0]], np.int32))
+    lo2 = _t(np.array([0, 1, 2, 3], np.int32))
+    a2, b2 = a.clone(), b.clone()
+    ivf.range_topk(ctx, xt, xn, xt, xn, blocks, lo2, ranges2, m, flags=f | 4, row_map=perm, out_ids=a2, out_dists=d1)
+    ivf.range_topk(ctx, xt, xn, xt, xn, blocks, lo2, ranges2, m, flags=f | 4, row_map=perm, out_ids=b2, out_dists=d2,
+                   rows_bf16=xb, cols_bf16=xb)
+    assert torch.equal(a2, b2) and torch.equal(d1, d2)
+
+
+def test_ivf_graph_tensor_cores_equal_cuda_cores(ctx):
+    from paper_2512_02278_b200 import ivf
+    graphs = []
+    for tc in (False, True):
+        xt = ivf.sift_like_device(40000, 96, rank=12, seed=5, device="cuda")
+        ctx.reset()
+        ivf.build_graph_ivf(ctx, xt, degree=32, cluster_size=512, probe=6, n_coarse=8, sample=40000, iters=3,
+                            optimize=True, keep=12, tensor_cores=tc)
+        graphs.append(ctx_adjacency(ctx, 40000, 32).copy())
+    assert np.array_equal(graphs[0], graphs[1])
+    ctx.reset()
