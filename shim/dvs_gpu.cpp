@@ -69,15 +69,18 @@ struct Backend {
       const unsigned char* c = static_cast<const unsigned char*>(p);
       for (std::size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ull;
     };
-    const std::size_t vb = g.vectors.data.size() * 4, ab = g.adjacency.size() * 4;
-    if (vb + ab <= (64u << 20)) {  // full content for small graphs
-      mix(g.vectors.data.data(), vb);
-      mix(g.adjacency.data(), ab);
-      mix(g.global_ids.data(), g.global_ids.size() * 4);
-    } else {                       // strided sample for large ones
-      for (std::size_t i = 0; i < g.vectors.data.size(); i += 4093) mix(&g.vectors.data[i], 4);
-      for (std::size_t i = 0; i < g.adjacency.size(); i += 4093) mix(&g.adjacency[i], 4);
-    }
+    // runs on every call (one query per call): a bounded sample -- the ends
+    // and ~1k evenly spaced elements of each array -- not the whole content
+    auto sample = [&](const auto& v) {
+      const std::size_t n = v.size();
+      if (n == 0) return;
+      const std::size_t step = n > 1024 ? n / 1024 : 1;
+      for (std::size_t i = 0; i < n; i += step) mix(&v[i], sizeof(v[0]));
+      for (std::size_t i = n > 64 ? n - 64 : 0; i < n; ++i) mix(&v[i], sizeof(v[0]));
+    };
+    sample(g.vectors.data);
+    sample(g.adjacency);
+    sample(g.global_ids);
     return h;
   }
   std::uint32_t ensure(const dvs::GraphIndex& g) {
