@@ -90,9 +90,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "=r"(r[30]), "=r"(r[31])                                                                             \
       : "r"(taddr))
 
-// smem per CTA: A (128 x K bf16) + 2 x B (128 x K bf16) + col norms x2 + lists
+// dynamic smem per CTA: A (128 x K bf16) + 2 x B (128 x K bf16) + lists + barrier
 __host__ __device__ inline size_t tc_smem_bytes(int kpad) {
-  return (size_t)3 * TCM * kpad * 2 + 2 * TCN * 4 + (size_t)32 * TCM * 8 + 64;
+  return (size_t)3 * TCM * kpad * 2 + (size_t)32 * TCM * 8 + 64;
 }
 
 __global__ void __launch_bounds__(128, 1)
@@ -103,11 +103,9 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
                      uint32_t* __restrict__ out_ids, float* __restrict__ out_dists, uint64_t out_stride) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sa = smem;
-  unsigned char* sb[2] = {smem + (size_t)TCM * kpad * 2, smem + (size_t)2 * TCM * kpad * 2};
-  float* cn[2];
-  cn[0] = reinterpret_cast<float*>(smem + (size_t)3 * TCM * kpad * 2);
-  cn[1] = cn[0] + TCN;
-  uint64_t* list = reinterpret_cast<uint64_t*>(cn[1] + TCN);  // [32][128]: entry j of row t at j*128 + t
+  auto sb = [&](int b) { return smem + (size_t)(1 + b) * TCM * kpad * 2; };  // B double buffer
+  __shared__ float cn[2][TCN];  // column norms of the two B tiles (static smem: LDS, not generic loads)
+  uint64_t* list = reinterpret_cast<uint64_t*>(smem + (size_t)3 * TCM * kpad * 2);  // [32][128]: entry j of row t at j*128 + t
   uint64_t* bar = list + 32 * TCM;
   __shared__ uint32_t tmem_slot;
 
@@ -172,7 +170,7 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
     for (int q = tid; q < TCN * kch; q += 128) {
       const int r = q / kch, kc = q - r * kch;
       const bool v = c + r < end;
-      cp16(s32(sb[buf] + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), cols + (uint64_t)(v ? c + r : 0) * kpad + kc * 8,
+      cp16(s32(sb(buf) + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), cols + (uint64_t)(v ? c + r : 0) * kpad + kc * 8,
            v);
     }
     cn[buf][tid] = c + tid < end ? cnorm[c + tid] : 0.f;
@@ -194,7 +192,7 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t abase = s32(sa), bbase = s32(sb[buf]);
+      const uint32_t abase = s32(sa), bbase = s32(sb(buf));
       for (int kk = 0; kk < kpad / 16; ++kk) {
         const uint64_t ad = umma_desc(abase + kk * 2 * lbo, lbo, sbo);
         const uint64_t bd = umma_desc(bbase + kk * 2 * lbo, lbo, sbo);

@@ -1,4 +1,4 @@
-"""K1 vs node-sharded search (bulk and fused exchange) with R ranks emulated on one GPU (protocol overhead
+"""K1 vs node-sharded search (bench workload, default cfg3; `--nq` to shrink) (bulk and fused exchange) with R ranks emulated on one GPU (protocol overhead
 without NVLink): K1 event time for the bench workload, plus parity."""
 import os
 import sys
@@ -9,13 +9,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2512_02278_b200 as dvs  # noqa: E402
 
-sys.argv = ["x"] + sys.argv[1:]
-args = bench.parse()
+import torch  # noqa: E402
+
+args = bench.parse(sys.argv[1:])
 ctx = dvs.Context(0)
-data, queries, index = bench.workload(args, 0, ctx)
-ctx.load_index(index)
+w = bench.build_workload(args, 0, ctx, torch.device("cuda", 0))
+queries = w.queries[:, :args.dim].cpu().numpy()
 ctx.set_timing(True)
-p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, accum=args.accum)
+p = dvs.SearchParams(args.iterations, args.beam, args.k, args.entry, metric=args.metric, accum=args.accum)
 ref = None
 for _ in range(2):
     ref = ctx.beam_search(0, queries, p)
