@@ -411,6 +411,12 @@ dvsg_status dvsg_last_timings(dvsg_ctx *ctx, float *search_ms, float *assign_ms,
                               float *combine_ms, float *total_ms);
 /* Number of library kernels launched by this context since creation. */
 uint64_t dvsg_kernel_launches(dvsg_ctx *ctx);
+/* Which K5 variant served the last assign_top_c / run_pipeline assign of
+ * this context: 0 warp kernel (C < 8), 1 exact fp64 tiles, 2 tensor cores
+ * (TF32 tcgen05 candidates + exact fp64 re-rank + certificate; *fallbacks =
+ * queries whose certificate failed and were finished by the exact kernel).
+ * -1 before any assign.  Results are identical on every path. */
+dvsg_status dvsg_last_assign_info(dvsg_ctx *ctx, int *path, uint64_t *fallbacks);
 /* Totals of the last K1 launch: units searched, vectors scored (the
  * reference's visited counter) and frontier nodes expanded -- the inputs of
  * the algorithmic byte count visited*4d + expanded*4*d_g + 4d per unit. */

@@ -316,6 +316,14 @@ class Context:
                                              ctypes.c_void_p(d_dists), ctypes.c_void_p(d_counts),
                                              ctypes.c_void_p(d_visited)))
 
+    def last_assign_info(self):
+        """(path, fallbacks) of the last assign: path 0 warp, 1 fp64 tiles,
+        2 tensor cores; fallbacks = queries the certificate sent to the exact
+        kernel (path 2 only)."""
+        path, fb = ctypes.c_int(), ctypes.c_uint64()
+        check(lib.dvsg_last_assign_info(self._h, ctypes.byref(path), ctypes.byref(fb)))
+        return int(path.value), int(fb.value)
+
     def assign_top_c(self, queries, c: int) -> np.ndarray:
         q = _f32(queries, 2)
         out = np.zeros((q.shape[0], max(int(c), 1)), np.uint32)

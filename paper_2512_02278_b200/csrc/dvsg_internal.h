@@ -164,10 +164,14 @@ size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_sme
 constexpr int kChunk = 8 * kThreads;  // raw candidates per dedup/score/merge chunk (8 per thread)
 
 // K5 assign (route_kernels.cu): nq x c cluster ids, exact fp64 expanded form.
-// scratch: nq x (clusters + 1) u64 (keys + query norms of the tiled large-C path).
+// scratch: assign_scratch_words(...) u64.  *path (nullable) = 0 warp kernel,
+// 1 fp64 tiles, 2 tensor cores (TF32 candidates + exact re-rank; word 0 of
+// the scratch then holds the number of queries the certificate sent to the
+// exact kernel).
+size_t assign_scratch_words(uint64_t nq, int dim, int clusters, int c);
 cudaError_t launch_assign(const float* queries, uint64_t nq, int dim, const float* cents,
                           const double* cent_norms, int clusters, int c, uint32_t* out,
-                          uint64_t* scratch, cudaStream_t stream);
+                          uint64_t* scratch, cudaStream_t stream, int* path = nullptr);
 // K4 combine: per query merge nparts sorted partial lists (stride entries each).
 cudaError_t launch_combine(uint64_t nq, int nparts, const uint32_t* ids, const float* dists,
                            const uint32_t* counts, int stride, int k, uint32_t* out_ids,
@@ -222,6 +226,11 @@ cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const
                                  const uint32_t* list_off, const uint2* ranges, int m, int flags, uint32_t* out_ids,
                                  float* out_dists, uint64_t out_stride, cudaStream_t stream);
 size_t range_topk_tc_smem_bytes(int kpad);
+// same over fp32 rows / cols read as tf32 (kind::tf32; kpad % 8 == 0, <= 128)
+cudaError_t launch_range_topk_tf32(const float* rows, const float* rnorm, const float* cols, const float* cnorm,
+                                   int kpad, const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks,
+                                   const uint32_t* list_off, const uint2* ranges, int m, int flags, uint32_t* out_ids,
+                                   float* out_dists, uint64_t out_stride, cudaStream_t stream);
 cudaError_t launch_to_bf16(const float* x, uint64_t n, int dpad, int kpad, uint16_t* out, cudaStream_t stream);
 cudaError_t launch_row_norms(const float* x, uint64_t n, int dpad, float* out, cudaStream_t stream);
 // Exact compute_entry_order on the device (dim <= 1024).

@@ -247,11 +247,21 @@ struct dvsg_ctx {
   float t_search = 0, t_assign = 0, t_combine = 0, t_total = 0;
   int timing_pending = 0;  // 1: search only, 2: pipeline
   std::atomic<uint64_t> launches{0};
+  int assign_path = -1;  // K5 variant of the last context assign (launch_assign's *path)
 };
 
 namespace {
 
+// kernels one launch_assign issues on each path (warp / fp64 tiles / tensor cores)
+uint64_t assign_launches(int path) { return path == 2 ? 7 : path == 1 ? 3 : 1; }
+
 void set_device(dvsg_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+// Synchronous-API copies and memsets run on the legacy default stream, which
+// is not ordered with the context's non-blocking streams (and a pageable
+// cudaMemcpy H2D may return before its DMA has landed): drain it before any
+// kernel on c->stream reads what they wrote.
+void legacy_fence() { cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "legacy stream"); }
 
 int32_t slot_of(const dvsg_ctx* c, uint32_t cluster) {
   for (size_t i = 0; i < c->parts.size(); ++i)
@@ -700,6 +710,7 @@ dvsg::XgView xg_view(unsigned char* region, const float* vec, uint64_t lo, int n
 void xg_check(dvsg_ctx* c) {
   if (!c->xg.issued) return;
   int err = 0;
+  cuda_check(cudaStreamSynchronize(c->stream), "sharded err");
   cuda_check(cudaMemcpy(&err, c->xg.err.p, sizeof err, cudaMemcpyDeviceToHost), "sharded err");
   c->xg.issued = false;
   if (err & 8) fail(DVSG_EINTERNAL, "sharded search: a peer rank did not reach the exchange barrier (20 s)");
@@ -1044,6 +1055,7 @@ void build_locator(dvsg_ctx* c) {
   if (!c->locator_dirty) return;
   // gid -> device row, over the resident partitions (simulator.cpp:275-288)
   std::vector<uint32_t> g(c->rows);
+  cuda_check(cudaStreamSynchronize(c->stream), "sync");
   if (c->rows) cuda_check(cudaMemcpy(g.data(), c->gids.p, c->rows * 4, cudaMemcpyDeviceToHost), "gids D2H");
   uint64_t total = 0;
   for (auto x : g) total = std::max<uint64_t>(total, (uint64_t)x + 1);
@@ -1085,11 +1097,11 @@ void pipeline_device(dvsg_ctx* c, const float* d_q, uint64_t nq, int dim, const 
   c->err_flag.reserve(1, c->stream);
   if (reset_err) cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
   if (c->timing) cudaEventRecord(c->ev[2], c->stream);
-  c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
-  cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->assign_scratch.p, c->stream), "assign");
+  c->assign_scratch.reserve(dvsg::assign_scratch_words(nq, dim, c->clusters, fanout), c->stream);
+  cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout, c->assign.p, c->assign_scratch.p, c->stream, &c->assign_path), "assign");
   cuda_check(dvsg::launch_route(c->assign.p, nq, fanout, c->d_cluster_slot.p, c->slot_map_n, c->unit_q.p, c->unit_p.p, c->err_flag.p, c->stream), "route");
   if (c->timing) cudaEventRecord(c->ev[3], c->stream);
-  c->launches += 2;
+  c->launches += assign_launches(c->assign_path) + 1;
   search_units(c, d_q, nq, dim, c->unit_q.p, c->unit_p.p, nu, p, c->u_ids.p, c->u_dists.p, c->u_count.p, vis);
   if (c->timing) cudaEventRecord(c->ev[4], c->stream);
   cuda_check(dvsg::launch_combine(nq, fanout, c->u_ids.p, c->u_dists.p, c->u_count.p, p->k, p->k, d_ids, d_dists, d_count, c->err_flag.p, c->stream), "combine");
@@ -1353,6 +1365,7 @@ dvsg_status dvsg_load_partition(dvsg_ctx* c, uint32_t cluster, uint64_t n, int d
     cuda_check(cudaMemcpy(c->adj.p + r0 * c->dg, adjacency, n * (uint64_t)c->dg * 4, cudaMemcpyHostToDevice), "adjacency H2D");
     cuda_check(cudaMemcpy(c->gids.p + r0, global_ids, n * 4, cudaMemcpyHostToDevice), "gids H2D");
     cuda_check(cudaMemcpy(c->entry.p + r0, entry_order, n * 4, cudaMemcpyHostToDevice), "entry H2D");
+    legacy_fence();
     c->parts.push_back(dvsg::PartDesc{r0, (uint32_t)n, cluster});
     c->part_mono.push_back(ids_increasing(global_ids, n));
     c->all_integral = c->all_integral && integral_all(vectors, n * (uint64_t)dim);
@@ -1381,6 +1394,7 @@ dvsg_status dvsg_get_entry_order(dvsg_ctx* c, uint32_t cluster, uint32_t* out) {
     const int32_t s = slot_of(c, cluster);
     if (s < 0) fail(DVSG_EINVAL, "cluster %u not resident", cluster);
     const auto& pd = c->parts[(size_t)s];
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
     cuda_check(cudaMemcpy(out, c->entry.p + pd.row_off, (size_t)pd.n * 4, cudaMemcpyDeviceToHost), "entry D2H");
   });
 }
@@ -1521,6 +1535,7 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
       cuda_check(cudaMemcpy(c->gids.p, io.data(), n_total * 4, cudaMemcpyHostToDevice), "gids H2D");
     }
     cuda_check(cudaMemcpy(c->entry.p, entry_order, n_total * 4, cudaMemcpyHostToDevice), "entry H2D");
+    legacy_fence();
     c->parts.push_back(dvsg::PartDesc{0, (uint32_t)n_total, 0});
     c->part_mono.push_back(global_ids ? ids_increasing(global_ids, n_total) : 1);
     c->all_integral = integral_all(shard_vectors, (hi - lo) * (uint64_t)dim);
@@ -1546,9 +1561,11 @@ dvsg_status dvsg_shard_init_resident(dvsg_ctx* c, int nranks, int rank) {
     const uint64_t rows = std::max<uint64_t>(hi - lo, 1);
     DevBuf<float> own;
     own.reserve(rows * (uint64_t)c->dpad, c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
     cuda_check(cudaMemset(own.p, 0, rows * (uint64_t)c->dpad * 4), "memset");
     if (hi > lo)
       cuda_check(cudaMemcpy(own.p, c->vec.p + lo * c->dpad, (hi - lo) * (uint64_t)c->dpad * 4, cudaMemcpyDeviceToDevice), "shard rows");
+    legacy_fence();
     std::swap(c->vec.p, own.p);
     std::swap(c->vec.cap, own.cap);
     c->parts[0].cluster = 0;
@@ -1578,6 +1595,7 @@ void shard_arena_setup(dvsg_ctx* c, int nranks, int rank, uint64_t n_total) {
   sh.arena_bytes = sh.xg_off + sh.xg_bytes;
   cuda_check(cudaMalloc(&sh.arena, sh.arena_bytes), "arena");
   cuda_check(cudaMemset(sh.arena, 0, sh.xg_off + kXgHeader), "arena reset");
+  legacy_fence();
   for (auto& e : c->xg.epoch) e = 0;
 }
 }  // namespace
@@ -1643,9 +1661,9 @@ dvsg_status dvsg_assign_top_c(dvsg_ctx* c, const float* queries, uint64_t nq, in
     if (!finite_all(queries, nq * (uint64_t)dim)) fail(DVSG_EINVAL, "Dataset: non-finite query element");
     const float* d_q = stage(c->io_f, queries, nq * (uint64_t)dim, c->stream);
     c->assign.reserve(nq * (uint64_t)cc, c->stream);
-    c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
-    cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, c->assign.p, c->assign_scratch.p, c->stream), "assign");
-    c->launches += 1;
+    c->assign_scratch.reserve(dvsg::assign_scratch_words(nq, dim, c->clusters, cc), c->stream);
+    cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, c->assign.p, c->assign_scratch.p, c->stream, &c->assign_path), "assign");
+    c->launches += assign_launches(c->assign_path);
     cuda_check(cudaMemcpyAsync(out, c->assign.p, nq * (uint64_t)cc * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
     cuda_check(cudaStreamSynchronize(c->stream), "assign");
   });
@@ -1659,9 +1677,9 @@ dvsg_status dvsg_assign_top_c_device(dvsg_ctx* c, const float* d_queries, uint64
     if (cc < 1 || cc > c->clusters) fail(DVSG_EINVAL, "assign_top_c: c=%d out of range for %d clusters", cc, c->clusters);
     if (dim != c->dim) fail(DVSG_EINVAL, "assign_top_c: query dim %d != centroid dim %d", dim, c->dim);
     if (nq == 0) return;
-    c->assign_scratch.reserve(nq * ((uint64_t)c->clusters + 1), c->stream);  // keys + query norms
-    cuda_check(dvsg::launch_assign(d_queries, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, d_out, c->assign_scratch.p, c->stream), "assign");
-    c->launches += 1;
+    c->assign_scratch.reserve(dvsg::assign_scratch_words(nq, dim, c->clusters, cc), c->stream);
+    cuda_check(dvsg::launch_assign(d_queries, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, cc, d_out, c->assign_scratch.p, c->stream, &c->assign_path), "assign");
+    c->launches += assign_launches(c->assign_path);
   });
 }
 
@@ -1867,6 +1885,7 @@ dvsg_status dvsg_build_graph(dvsg_ctx* c, const float* vectors, uint64_t n, int 
     da.reserve(n * (uint64_t)out_degree, c->stream);
     cuda_check(cudaMemset(dv.p, 0, n * (uint64_t)dpad * 4), "memset");
     cuda_check(cudaMemcpy2D(dv.p, (size_t)dpad * 4, vectors, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "H2D");
+    legacy_fence();
     cuda_check(dvsg::launch_knn_build(dv.p, n, dim, dpad, out_degree, da.p, c->stream), "knn build");
     c->launches += 1;
     cuda_check(cudaStreamSynchronize(c->stream), "knn build");
@@ -1895,6 +1914,7 @@ dvsg_status dvsg_brute_force_topk(dvsg_ctx* c, const float* db, uint64_t n, int 
     cuda_check(cudaMemset(dq.p, 0, nq * (uint64_t)dpad * 4), "memset");
     cuda_check(cudaMemcpy2D(dd.p, (size_t)dpad * 4, db, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy2D(dq.p, (size_t)dpad * 4, queries, (size_t)dim * 4, (size_t)dim * 4, nq, cudaMemcpyHostToDevice), "H2D");
+    legacy_fence();
     cuda_check(dvsg::launch_brute_force(dq.p, nq, dd.p, n, dpad, k, oi.p, od.p, c->stream), "brute force");
     c->launches += 1;
     cuda_check(cudaStreamSynchronize(c->stream), "brute force");
@@ -2029,6 +2049,7 @@ dvsg_status dvsg_partition_alloc_device(dvsg_ctx* c, uint32_t cluster, uint64_t 
     c->dpad = dpad;
     c->dg = out_degree;
     if (dpad != dim) cuda_check(cudaMemset(c->vec.p + r0 * dpad, 0, n * (uint64_t)dpad * 4), "pad");
+    legacy_fence();
     c->pend = dvsg_ctx::Pending{true, cluster, n, r0};
     if (d_vectors) *d_vectors = c->vec.p + r0 * dpad;
     if (d_adjacency) *d_adjacency = c->adj.p + r0 * out_degree;
@@ -2131,13 +2152,16 @@ std::vector<double> center_norms(const std::vector<float>& cents, int clusters, 
 // that keep K5's (rows x clusters) key scratch under 512 MB
 void assign_nearest(dvsg_ctx* c, const float* d_x, uint64_t n, int dim, const float* d_cents,
                     const double* d_norms, int clusters, uint32_t* d_labels, DevBuf<uint64_t>& scratch) {
-  const uint64_t chunk = std::max<uint64_t>(1024, (512ull << 20) / (8ull * (uint64_t)(clusters + 1)));
-  scratch.reserve(std::min<uint64_t>(chunk, n) * (uint64_t)(clusters + 1), c->stream);
+  uint64_t chunk = std::max<uint64_t>(1024, (512ull << 20) / (8ull * (uint64_t)(clusters + 1)));
+  if (dvsg::assign_scratch_words(chunk, dim, clusters, 1) < chunk * (uint64_t)(clusters + 1))
+    chunk = std::max<uint64_t>(chunk, 1ull << 20);  // tensor-core path: O(rows x dim) scratch
+  scratch.reserve(dvsg::assign_scratch_words(std::min<uint64_t>(chunk, n), dim, clusters, 1), c->stream);
   for (uint64_t b = 0; b < n; b += chunk) {
     const uint64_t m = std::min<uint64_t>(chunk, n - b);
+    int path = 0;
     cuda_check(dvsg::launch_assign(d_x + b * (uint64_t)dim, m, dim, d_cents, d_norms, clusters, 1, d_labels + b,
-                                   scratch.p, c->stream), "assign");
-    c->launches += 1;
+                                   scratch.p, c->stream, &path), "assign");
+    c->launches += assign_launches(path);
   }
 }
 
@@ -2430,6 +2454,7 @@ dvsg_status dvsg_cluster_comm_init(dvsg_ctx* c, int nranks, int rank, uint64_t m
       if ((int)r >= nranks) fail(DVSG_EINVAL, "cluster_comm_init: placement names rank %u of %d", r, nranks);
     c->cl_place.reserve(place.size(), c->stream);
     cuda_check(cudaMemcpy(c->cl_place.p, place.data(), place.size() * 4, cudaMemcpyHostToDevice), "placement");
+    legacy_fence();
     cl.active = true;
   });
 }
@@ -2504,9 +2529,9 @@ dvsg_status dvsg_run_pipeline_cluster_device(dvsg_ctx* c, const float* d_q, uint
     cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), s), "err reset");
     // assign (K5) -> dispatch (K3, peer stores) -> barrier
     c->assign.reserve(std::max<uint64_t>(nu, 1), s);
-    c->assign_scratch.reserve(std::max<uint64_t>(nq, 1) * ((uint64_t)c->clusters + 1), s);
+    c->assign_scratch.reserve(dvsg::assign_scratch_words(nq, dim, c->clusters, fanout), s);
     if (nq) cuda_check(dvsg::launch_assign(d_q, nq, dim, c->d_cents.p, c->d_cent_norms.p, c->clusters, fanout,
-                                           c->assign.p, c->assign_scratch.p, s), "assign");
+                                           c->assign.p, c->assign_scratch.p, s, &c->assign_path), "assign");
     cuda_check(dvsg::launch_cl_dispatch(c->cl_peers.p, cl.nranks, cl.rank, cl.parity, d_q, nq, dim, fanout,
                                         c->assign.p, c->cl_place.p, (uint32_t)c->clusters, cl.cap, c->cl_err.p, s),
                "dispatch");
@@ -2628,6 +2653,21 @@ dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, f
 }
 
 uint64_t dvsg_kernel_launches(dvsg_ctx* c) { return c ? c->launches.load() : 0; }
+
+dvsg_status dvsg_last_assign_info(dvsg_ctx* c, int* path, uint64_t* fallbacks) {
+  return guarded([&] {
+    if (path) *path = c->assign_path;
+    if (fallbacks) {
+      *fallbacks = 0;
+      if (c->assign_path == 2) {
+        uint32_t n = 0;
+        cuda_check(cudaStreamSynchronize(c->stream), "assign info");
+        cuda_check(cudaMemcpy(&n, c->assign_scratch.p, sizeof(n), cudaMemcpyDeviceToHost), "assign info");
+        *fallbacks = n;
+      }
+    }
+  });
+}
 
 dvsg_status dvsg_debug_counters(dvsg_ctx* c, uint64_t* out16) {
   return guarded([&] {

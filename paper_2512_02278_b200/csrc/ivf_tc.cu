@@ -11,8 +11,14 @@
 // issued by one thread (tcgen05.mma.cta_group::1.kind::f16, M=128, N=128,
 // K=16 per instruction) and committed to an mbarrier; the 4 warps then read
 // their 32 TMEM lanes (tcgen05.ld 32x32b.x32), form dist = |x|^2 + |y|^2 -
-// 2 x.y and keep a per-thread sorted top-m list in shared memory.  The next
-// column tile streams in while the current one is multiplied and scanned.
+// 2 x.y and filter them against their row's current m-th key into a
+// per-row survivor buffer in shared memory (one predicated store per column,
+// no divergent loop); each warp then merges the survivors of its 32 rows into
+// register-resident sorted lists (lane i of the warp holds the i-th smallest
+// key of each of its rows: one ballot + shuffle per insertion, whatever the
+// position -- a per-thread sorted insert diverges across the warp and cost 8x
+// the instructions).  The next column tile streams in while the current one
+// is multiplied and scanned.
 //
 // Exactness: the bench data are integers in [0, 255]: exact in bf16, every
 // product exact in fp32 and every partial sum an integer below 2^24, so the
@@ -90,30 +96,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "=r"(r[30]), "=r"(r[31])                                                                             \
       : "r"(taddr))
 
-// dynamic smem per CTA: A (128 x K bf16) + 2 x B (128 x K bf16) + lists + barrier
-__host__ __device__ inline size_t tc_smem_bytes(int kpad) {
-  return (size_t)3 * TCM * kpad * 2 + (size_t)32 * TCM * 8 + 64;
+// dynamic smem per CTA: A (128 x K) + 2 x B (128 x K) + survivor buffer + barrier
+__host__ __device__ inline size_t tc_smem_bytes(int row_bytes) {
+  return (size_t)3 * TCM * row_bytes + (size_t)32 * TCM * 8 + 64;
 }
 
+// T = uint16_t: bf16 operands (kind::f16, K = 16 per MMA); T = float: tf32
+// operands read from fp32 storage (kind::tf32, K = 8 per MMA).  Either way one
+// MMA consumes a 32-byte K slice of every row.
+template <typename T>
 __global__ void __launch_bounds__(128, 1)
-range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict__ rnorm,
-                     const uint16_t* __restrict__ cols, const float* __restrict__ cnorm, int kpad,
+range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm,
+                     const T* __restrict__ cols, const float* __restrict__ cnorm, int kpad,
                      const uint32_t* __restrict__ row_map, const RangeBlock* __restrict__ blocks,
                      const uint32_t* __restrict__ list_off, const uint2* __restrict__ ranges, int m, int flags,
                      uint32_t* __restrict__ out_ids, float* __restrict__ out_dists, uint64_t out_stride) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* sa = smem;
-  auto sb = [&](int b) { return smem + (size_t)(1 + b) * TCM * kpad * 2; };  // B double buffer
+  constexpr bool kTF32 = sizeof(T) == 4;
+  constexpr int kEl = 16 / sizeof(T);  // elements per 16-byte chunk
+  const int row_bytes = kpad * (int)sizeof(T);
+  auto sb = [&](int b) { return smem + (size_t)(1 + b) * TCM * row_bytes; };  // B double buffer
   __shared__ float cn[2][TCN];  // column norms of the two B tiles (static smem: LDS, not generic loads)
-  uint64_t* list = reinterpret_cast<uint64_t*>(smem + (size_t)3 * TCM * kpad * 2);  // [32][128]: entry j of row t at j*128 + t
-  uint64_t* bar = list + 32 * TCM;
+  uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + (size_t)3 * TCM * row_bytes);  // [32][128]: survivor j of row t at j*128 + t
+  uint64_t* bar = cbuf + 32 * TCM;
   __shared__ uint32_t tmem_slot;
 
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const RangeBlock blk = blocks[blockIdx.x];
   const int nrows = (int)blk.nrows;
-  const uint32_t lbo = 128, sbo = (uint32_t)(kpad / 8) * 128;
-  const int kch = kpad / 8;  // 16-byte chunks per row
+  const int kch = row_bytes / 16;  // 16-byte chunks per row
+  const uint32_t lbo = 128, sbo = (uint32_t)kch * 128;
 
   // ---- TMEM (128 fp32 columns) and the MMA-completion barrier
   if (warp == 0) {
@@ -127,27 +140,42 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
 
-  // ---- this thread's row: physical index, norm, list
+  // ---- this thread's row: physical index, norm; the warp's 32 row lists
   const bool rvalid = tid < nrows;
   const uint32_t prow = rvalid ? (row_map ? row_map[blk.row0 + tid] : blk.row0 + tid) : 0u;
   const float nr = rvalid ? rnorm[prow] : 0.f;
   const uint64_t orow = (flags & 8) ? (uint64_t)prow : (uint64_t)blk.out_row0 + (uint64_t)tid;
-  int cnt = 0;
-  if ((flags & 4) && rvalid) {  // continue from the lists already in the output
-    for (int j = 0; j < m; ++j) {
-      const uint32_t id = out_ids[orow * out_stride + j];
-      if (id == 0xFFFFFFFFu) break;
-      list[j * TCM + tid] = ((uint64_t)f2ord(out_dists[orow * out_stride + j]) << 32) | id;
-      cnt = j + 1;
+  uint64_t top[32];  // top[rr] at lane i: i-th smallest key of row warp*32 + rr
+  // this thread's row: current m-th key -- (+inf, 0) while the list is
+  // short, so the padding columns (+inf) never pass
+  const uint64_t kInfKey = (uint64_t)f2ord(__int_as_float(0x7F800000)) << 32;
+  uint64_t thr = kInfKey;
+  auto set_thr = [&](uint64_t t) { thr = t == ~0ull ? kInfKey : t; };
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    top[rr] = ~0ull;
+    if (flags & 4) {  // continue from the lists already in the output
+      const uint64_t o = __shfl_sync(0xFFFFFFFFu, orow, rr);
+      const bool v = __shfl_sync(0xFFFFFFFFu, rvalid, rr);
+      uint32_t id = 0xFFFFFFFFu;
+      float d = 0.f;
+      if (v && lane < m) {
+        id = out_ids[o * out_stride + lane];
+        d = out_dists[o * out_stride + lane];
+      }
+      const unsigned bad = __ballot_sync(0xFFFFFFFFu, id == 0xFFFFFFFFu);
+      const int first_bad = bad ? __ffs(bad) - 1 : 32;  // entries after the first gap are ignored
+      if (lane < first_bad) top[rr] = ((uint64_t)f2ord(d) << 32) | id;
+      const uint64_t t = __shfl_sync(0xFFFFFFFFu, top[rr], m - 1);
+      if (lane == rr) set_thr(t);
     }
   }
-  uint64_t thr = cnt == m ? list[(m - 1) * TCM + tid] : ~0ull;
 
   // ---- A: the block's rows, canonical K-major layout
   for (int c = tid; c < TCM * kch; c += 128) {
     const int r = c / kch, kc = c - r * kch;
     const uint32_t pr = r < nrows ? (row_map ? row_map[blk.row0 + r] : blk.row0 + r) : 0u;
-    cp16(s32(sa + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), rows + (uint64_t)pr * kpad + kc * 8, r < nrows);
+    cp16(s32(sa + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), rows + (uint64_t)pr * kpad + kc * kEl, r < nrows);
   }
   cp_commit();
 
@@ -170,19 +198,21 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
     for (int q = tid; q < TCN * kch; q += 128) {
       const int r = q / kch, kc = q - r * kch;
       const bool v = c + r < end;
-      cp16(s32(sb(buf) + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), cols + (uint64_t)(v ? c + r : 0) * kpad + kc * 8,
+      cp16(s32(sb(buf) + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), cols + (uint64_t)(v ? c + r : 0) * kpad + kc * kEl,
            v);
     }
-    cn[buf][tid] = c + tid < end ? cnorm[c + tid] : 0.f;
+    cn[buf][tid] = c + tid < end ? cnorm[c + tid] : __int_as_float(0x7F800000);  // +inf: never a survivor
     cp_commit();
   };
   if (have) load_b(0, li, c0);
-  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TCN >> 3) << 17) | ((uint32_t)(TCM >> 4) << 24);
+  // instruction descriptor: D f32, A/B bf16 (1) or tf32 (2), K-major, N, M
+  const uint32_t fmt = kTF32 ? 2u : 1u;
+  const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TCN >> 3) << 17) | ((uint32_t)(TCM >> 4) << 24);
 
   int buf = 0;
   uint32_t phase = 0;
   while (have) {
-    const uint32_t tl = li, tc = c0, tend = ranges[tl].y;
+    const uint32_t tc = c0;
     // prefetch the following tile into the other buffer (its MMA finished last round)
     uint32_t nl = li, nc = c0 + TCN;
     const bool nhave = next_tile(nl, nc);
@@ -193,15 +223,23 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t abase = s32(sa), bbase = s32(sb(buf));
-      for (int kk = 0; kk < kpad / 16; ++kk) {
+      for (int kk = 0; kk < row_bytes / 32; ++kk) {
         const uint64_t ad = umma_desc(abase + kk * 2 * lbo, lbo, sbo);
         const uint64_t bd = umma_desc(bbase + kk * 2 * lbo, lbo, sbo);
         const uint32_t acc = kk > 0 ? 1u : 0u;
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-            "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-            : "memory");
+        if constexpr (kTF32) {
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+              : "memory");
+        } else {
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+              "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+              : "memory");
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
                    : "memory");
@@ -209,36 +247,46 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
     mbar_wait(bar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // ---- epilogue: this thread's row, 128 columns in 4 TMEM loads of 32
-    float thr_d = thr == ~0ull ? __int_as_float(0x7F800000) : ord2f((uint32_t)(thr >> 32));
+    // ---- epilogue: 128 columns in 4 TMEM loads of 32
 #pragma unroll 1
     for (int part = 0; part < TCN / 32; ++part) {
       uint32_t r[32];
       TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(part * 32), r);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (!rvalid) continue;
+      // (1) this thread's row: survivors of the m-th-key filter -> cbuf
+      int ns = 0;
+      if (rvalid) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int cl = part * 32 + j;
-        const uint32_t col = tc + (uint32_t)cl;
-        const float dist = fmaxf(fmaf(-2.f, __uint_as_float(r[j]), nr + cn[buf][cl]), 0.f);
-        if (dist > thr_d || col >= tend) continue;
-        if ((flags & 1) && col == prow) continue;
-        const uint64_t key = ((uint64_t)f2ord(dist) << 32) | col;
-        if (key >= thr) continue;
-        // sorted insert into the thread's list (rare after the first tiles)
-        int pos = cnt < m ? cnt : m - 1;
-        while (pos > 0 && list[(pos - 1) * TCM + tid] > key) {
-          list[pos * TCM + tid] = list[(pos - 1) * TCM + tid];
-          --pos;
-        }
-        list[pos * TCM + tid] = key;
-        if (cnt < m) ++cnt;
-        if (cnt == m) {
-          thr = list[(m - 1) * TCM + tid];
-          thr_d = ord2f((uint32_t)(thr >> 32));
+        for (int j = 0; j < 32; ++j) {
+          const int cl = part * 32 + j;
+          const uint32_t col = tc + (uint32_t)cl;
+          const float dist = fmaxf(fmaf(-2.f, __uint_as_float(r[j]), nr + cn[buf][cl]), 0.f);
+          const uint64_t key = ((uint64_t)f2ord(dist) << 32) | col;
+          const bool ok = key < thr && !((flags & 1) && col == prow);
+          if (ok) cbuf[ns * TCM + tid] = key;
+          ns += ok ? 1 : 0;
         }
       }
+      __syncwarp();
+      // (2) the warp merges each of its rows' survivors into the row's list
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) {
+        const int n = __shfl_sync(0xFFFFFFFFu, ns, rr);
+        if (n == 0) continue;
+        const int row = warp * 32 + rr;
+        for (int s2 = 0; s2 < n; ++s2) {
+          const uint64_t key = cbuf[s2 * TCM + row];
+          const unsigned gt = __ballot_sync(0xFFFFFFFFu, top[rr] > key);
+          if (gt == 0) continue;  // not among the 32 smallest
+          const int pos = __ffs(gt) - 1;
+          const uint64_t up = __shfl_up_sync(0xFFFFFFFFu, top[rr], 1);
+          if (lane > pos) top[rr] = up;
+          if (lane == pos) top[rr] = key;
+        }
+        const uint64_t t = __shfl_sync(0xFFFFFFFFu, top[rr], m - 1);
+        if (lane == rr) set_thr(t);
+      }
+      __syncwarp();
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();  // TMEM and buffer `buf` free for the next round
@@ -248,22 +296,23 @@ range_topk_tc_kernel(const uint16_t* __restrict__ rows, const float* __restrict_
     have = nhave;
   }
 
-  // ---- emit (same rules as range_topk_kernel)
-  if (rvalid) {
+  // ---- emit (same rules as range_topk_kernel): lane j writes entry j of each row
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    if (!__shfl_sync(0xFFFFFFFFu, rvalid, rr)) continue;
+    const uint64_t o = __shfl_sync(0xFFFFFFFFu, orow, rr);
+    const int nv = __popc(__ballot_sync(0xFFFFFFFFu, lane < m && top[rr] != ~0ull));
     if (flags & 2) {
-      const int nv = cnt < m ? cnt : m;
-      for (int j = 0; j < m; ++j) {
-        const uint64_t kj = nv > 0 ? list[(j % nv) * TCM + tid] : 0ull;
-        out_ids[orow * out_stride + j] = nv > 0 ? (uint32_t)kj : prow;
-        if (out_dists) out_dists[orow * out_stride + j] = nv > 0 ? ord2f((uint32_t)(kj >> 32)) : 0.f;
+      const uint32_t pr = __shfl_sync(0xFFFFFFFFu, prow, rr);
+      const uint64_t kj = __shfl_sync(0xFFFFFFFFu, top[rr], nv > 0 ? lane % nv : 0);
+      if (lane < m) {
+        out_ids[o * out_stride + lane] = nv > 0 ? (uint32_t)kj : pr;
+        if (out_dists) out_dists[o * out_stride + lane] = nv > 0 ? ord2f((uint32_t)(kj >> 32)) : 0.f;
       }
-    } else {
-      for (int j = 0; j < m; ++j) {
-        const bool ok = j < cnt;
-        const uint64_t kj = ok ? list[j * TCM + tid] : 0ull;
-        out_ids[orow * out_stride + j] = ok ? (uint32_t)kj : 0xFFFFFFFFu;
-        if (out_dists) out_dists[orow * out_stride + j] = ok ? ord2f((uint32_t)(kj >> 32)) : __int_as_float(0x7F800000);
-      }
+    } else if (lane < m) {
+      const bool ok = lane < nv;
+      out_ids[o * out_stride + lane] = ok ? (uint32_t)top[rr] : 0xFFFFFFFFu;
+      if (out_dists) out_dists[o * out_stride + lane] = ok ? ord2f((uint32_t)(top[rr] >> 32)) : __int_as_float(0x7F800000);
     }
   }
   __syncthreads();
@@ -285,24 +334,44 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, uint64_t n, int dpad
 
 }  // namespace
 
-size_t range_topk_tc_smem_bytes(int kpad) { return tc_smem_bytes(kpad); }
+size_t range_topk_tc_smem_bytes(int kpad) { return tc_smem_bytes(kpad * 2); }
+
+template <typename T>
+cudaError_t launch_tc_t(const T* rows, const float* rnorm, const T* cols, const float* cnorm, int kpad,
+                        const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks, const uint32_t* list_off,
+                        const uint2* ranges, int m, int flags, uint32_t* out_ids, float* out_dists,
+                        uint64_t out_stride, cudaStream_t stream) {
+  const int row_bytes = kpad * (int)sizeof(T);
+  if (m < 1 || m > 32 || row_bytes % 32 || kpad < 1 || row_bytes > TCMAXK * 2) return cudaErrorInvalidValue;
+  if (nblocks == 0) return cudaSuccess;
+  const size_t smem = tc_smem_bytes(row_bytes);
+  cudaError_t e = cudaFuncSetAttribute(range_topk_tc_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  for (uint64_t b0 = 0; b0 < nblocks; b0 += 0x7FFFFFFFull) {
+    const uint64_t nb = nblocks - b0 < 0x7FFFFFFFull ? nblocks - b0 : 0x7FFFFFFFull;
+    range_topk_tc_kernel<T><<<(unsigned)nb, 128, smem, stream>>>(rows, rnorm, cols, cnorm, kpad, row_map, blocks + b0,
+                                                                 list_off, ranges, m, flags, out_ids, out_dists,
+                                                                 out_stride);
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const uint16_t* cols, const float* cnorm,
                                  int kpad, const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks,
                                  const uint32_t* list_off, const uint2* ranges, int m, int flags, uint32_t* out_ids,
                                  float* out_dists, uint64_t out_stride, cudaStream_t stream) {
-  if (m < 1 || m > 32 || kpad % 16 || kpad < 16 || kpad > TCMAXK) return cudaErrorInvalidValue;
-  if (nblocks == 0) return cudaSuccess;
-  const size_t smem = tc_smem_bytes(kpad);
-  cudaError_t e = cudaFuncSetAttribute(range_topk_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  for (uint64_t b0 = 0; b0 < nblocks; b0 += 0x7FFFFFFFull) {
-    const uint64_t nb = nblocks - b0 < 0x7FFFFFFFull ? nblocks - b0 : 0x7FFFFFFFull;
-    range_topk_tc_kernel<<<(unsigned)nb, 128, smem, stream>>>(rows, rnorm, cols, cnorm, kpad, row_map, blocks + b0,
-                                                              list_off, ranges, m, flags, out_ids, out_dists,
-                                                              out_stride);
-  }
-  return cudaGetLastError();
+  if (kpad % 16) return cudaErrorInvalidValue;
+  return launch_tc_t<uint16_t>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
+                               out_ids, out_dists, out_stride, stream);
+}
+
+cudaError_t launch_range_topk_tf32(const float* rows, const float* rnorm, const float* cols, const float* cnorm,
+                                   int kpad, const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks,
+                                   const uint32_t* list_off, const uint2* ranges, int m, int flags, uint32_t* out_ids,
+                                   float* out_dists, uint64_t out_stride, cudaStream_t stream) {
+  if (kpad % 8) return cudaErrorInvalidValue;
+  return launch_tc_t<float>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
+                            out_ids, out_dists, out_stride, stream);
 }
 
 cudaError_t launch_to_bf16(const float* x, uint64_t n, int dpad, int kpad, uint16_t* out, cudaStream_t stream) {
