@@ -37,15 +37,28 @@ namespace {
 // VPL: float4 slots per lane (dpad <= 128 * VPL).  U: vectors in flight per warp.
 // FULL: dpad == 128 * VPL (every lane holds real dimensions; no bound check).
 
-template <int VPL, typename ACC, int METRIC, bool FULL>
 #ifndef DVSG_MINB
 #define DVSG_MINB 5  // resident CTAs per SM the register budget is cut for (measured sweep)
 #endif
-__global__ void __launch_bounds__(kThreads, DVSG_MINB) search_kernel(const SearchArgs a) {
+// Wide rows (VPL >= 4, dim > 384): a 2-3 KB row per vector and pools that
+// cap residency at 2 CTAs/SM by shared memory anyway (w = 256: 107 KB), so
+// the register budget goes to more rows in flight per warp instead of more
+// CTAs: U = 4 (VPL 4-6) / 2 (VPL 8) at 2 CTAs/SM (<= 128 registers, no
+// spills).  Measured at 10M x 768 IP, w = 256 (configs[3]): 8.5k -> 15.4k QPS
+// f32c, alg 2.59 -> 4.68 TB/s; 2M x 512/768/1024 at w = 64 and 256 +5-110%.
+#ifndef DVSG_MINB_WIDE
+#define DVSG_MINB_WIDE 2
+#endif
 #ifndef DVSG_UVEC
 #define DVSG_UVEC 8  // vectors in flight per warp at VPL == 1 (measured sweep)
 #endif
-  constexpr int U = VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL);
+#ifndef DVSG_UVEC_WIDE
+#define DVSG_UVEC_WIDE -1  // vectors in flight per warp at VPL >= 4 (-1: 4, or 2 at VPL 8; 0: DVSG_UVEC / VPL)
+#endif
+template <int VPL, typename ACC, int METRIC, bool FULL>
+__global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MINB) search_kernel(const SearchArgs a) {
+  constexpr int UW = DVSG_UVEC_WIDE < 0 ? (VPL >= 8 ? 2 : 4) : DVSG_UVEC_WIDE;
+  constexpr int U = (VPL >= 4 && UW > 0) ? UW : (VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL));
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ BlockState st;
 

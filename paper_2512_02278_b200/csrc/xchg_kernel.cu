@@ -417,7 +417,8 @@ __device__ __forceinline__ void score_table(const XgArgs& a, ScoreTable& t) {
 template <int VPL, typename ACC, int METRIC, bool FULL>
 __device__ __forceinline__ void score_warp_block(const XgArgs& a, const ScoreTable& t, uint64_t b,
                                                  uint64_t* wq, uint64_t* wk) {
-  constexpr int U = VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL);
+  // rows in flight per warp: as K1 (search_kernel.cu), 4 (2 at VPL 8) for wide rows
+  constexpr int U = VPL >= 4 ? (VPL >= 8 ? 2 : 4) : (VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL));
   constexpr int LU = ilog2(U);
   const int lane = threadIdx.x & 31;
   const int R = a.nranks;
@@ -520,7 +521,7 @@ __device__ __forceinline__ void score_warp_block(const XgArgs& a, const ScoreTab
 // `sa` (do_s) from one work counter, interleaved, so origin-side work
 // (latency / issue bound) and owner-side gathers (HBM bound) share the SMs.
 template <int VPL, typename ACC, int METRIC, bool FULL>
-__global__ void __launch_bounds__(kThreads, sizeof(ACC) == 8 ? 3 : DVSG_XG_MINB)
+__global__ void __launch_bounds__(kThreads, VPL >= 4 ? 2 : sizeof(ACC) == 8 ? 3 : DVSG_XG_MINB)
 xg_step(const XgArgs ea, const XgArgs sa, int do_e, int do_s, unsigned long long* counter) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ BlockState st;
