@@ -679,7 +679,10 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 // ---- node-sharded search, bulk-synchronous exchange (xchg_kernel.cu) -------
 constexpr size_t kXgHeader = 256;  // cursor [2][8] u32 @0, flags [8] u32 @64
-constexpr int kXgLanes = 4;
+// Two query waves half a phase apart: every xg_step launch carries exactly one
+// expand op and one score op, so more lanes would need several of each per
+// launch (a third lane's op would collide with lane 0's parity) -- capped.
+constexpr int kXgLanes = 2;
 constexpr size_t kXgTlMax = 1024;  // timeline intervals kept per search
 
 size_t xg_region_bytes(int nranks, uint64_t wcap, uint64_t maxraw, int dpad) {
@@ -1479,6 +1482,11 @@ dvsg_status dvsg_beam_search_sharded_emulated(dvsg_ctx* c, int nranks, const flo
     c->u_dists.reserve(nq * k, c->stream);
     c->u_count.reserve(nq, c->stream);
     c->u_visited.reserve(nq, c->stream);
+    // diagnostic path: poison the outputs so a skipped query cannot pass as an
+    // earlier search's result left in the shared staging buffers
+    cuda_check(cudaMemsetAsync(c->u_ids.p, 0xFF, nq * k * 4, c->stream), "poison");
+    cuda_check(cudaMemsetAsync(c->u_count.p, 0xFF, nq * 4, c->stream), "poison");
+    cuda_check(cudaMemsetAsync(c->u_visited.p, 0xFF, nq * 8, c->stream), "poison");
     if (use_bulk_exchange(c)) search_xchg(c, true, nranks, d_q, nq, dim, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
     else search_sharded(c, true, nranks, d_q, nq, dim, p, c->u_ids.p, c->u_dists.p, c->u_count.p, c->u_visited.p);
     cuda_check(cudaMemcpyAsync(out_ids, c->u_ids.p, nq * k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
