@@ -417,6 +417,12 @@ uint64_t dvsg_kernel_launches(dvsg_ctx *ctx);
  * queries whose certificate failed and were finished by the exact kernel).
  * -1 before any assign.  Results are identical on every path. */
 dvsg_status dvsg_last_assign_info(dvsg_ctx *ctx, int *path, uint64_t *fallbacks);
+/* How the last dvsg_build_graph / dvsg_brute_force_topk of this context ran:
+ * *exact_mode 0 = fp32 tiles (byte-like data: every squared distance an exact
+ * fp32 integer), 1 = fp32 candidates + fp64 re-rank + certificate (any float
+ * data); *fallbacks = rows the certificate sent to the fp64 full scan.  -1
+ * before any call.  Results equal the reference's either way. */
+dvsg_status dvsg_last_knn_info(dvsg_ctx *ctx, int *exact_mode, uint64_t *fallbacks);
 /* Totals of the last K1 launch: units searched, vectors scored (the
  * reference's visited counter) and frontier nodes expanded -- the inputs of
  * the algorithmic byte count visited*4d + expanded*4*d_g + 4d per unit. */

@@ -324,6 +324,13 @@ class Context:
         check(lib.dvsg_last_assign_info(self._h, ctypes.byref(path), ctypes.byref(fb)))
         return int(path.value), int(fb.value)
 
+    def last_knn_info(self):
+        """(exact_mode, fallbacks) of the last build_graph / brute_force_topk:
+        0 fp32 tiles, 1 fp32 candidates + fp64 re-rank + certificate."""
+        mode, fb = ctypes.c_int(), ctypes.c_uint64()
+        check(lib.dvsg_last_knn_info(self._h, ctypes.byref(mode), ctypes.byref(fb)))
+        return int(mode.value), int(fb.value)
+
     def assign_top_c(self, queries, c: int) -> np.ndarray:
         q = _f32(queries, 2)
         out = np.zeros((q.shape[0], max(int(c), 1)), np.uint32)

@@ -301,5 +301,13 @@ cudaError_t launch_cl_barrier(const ClArena* peers, int nranks, int me, unsigned
 // K6 exact kNN graph rows (knn_build.cu)
 cudaError_t launch_knn_build(const float* vectors, uint64_t n, int dim, int dpad,
                              int out_degree, uint32_t* adjacency, cudaStream_t stream);
+// K6 exact on any float data: fp32 tiles keep 32 candidates + a lower bound of
+// the rest, fp64 re-rank + certificate, fp64 full scan of rejected rows.
+// build: rows == cols (graph rows, self excluded, cyclic padding); else brute
+// force (ids + dists, deg <= n).  scratch: knn_exact_scratch_bytes(nrows).
+size_t knn_exact_scratch_bytes(uint64_t nrows);
+cudaError_t launch_knn_exact(const float* rowv, uint64_t nrows, const float* vec, uint64_t n, int dim, int dpad,
+                             int deg, bool build, uint32_t* out_ids, float* out_dists, void* scratch,
+                             cudaStream_t stream);
 
 }  // namespace dvsg

@@ -124,6 +124,31 @@ bool integral_all(const float* x, uint64_t n) {
   return true;
 }
 
+// K6's fp32 tile distances equal the reference's fp64-then-rounded ones when
+// every coordinate is an integer and every squared distance stays below 2^24
+// (each partial sum an exact fp32 integer); otherwise the exact mode runs.
+bool k6_fp32_exact(const float* x, uint64_t rows, int dim, float* lo_out = nullptr, float* hi_out = nullptr) {
+  float lo = INFINITY, hi = -INFINITY;
+  const uint64_t n = rows * (uint64_t)dim;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (x[i] != std::nearbyint(x[i])) return false;
+    lo = std::min(lo, x[i]);
+    hi = std::max(hi, x[i]);
+  }
+  if (lo_out) *lo_out = lo;
+  if (hi_out) *hi_out = hi;
+  const double span = n ? (double)hi - (double)lo : 0.0;  // |x_i - y_i| <= span
+  return span * span * (double)dim < 16777216.0;
+}
+
+// both operands of a brute-force search: the span covers the union of their ranges
+bool k6_fp32_exact2(const float* a, uint64_t na, const float* b, uint64_t nb, int dim) {
+  float la, ha, lb, hb;
+  if (!k6_fp32_exact(a, na, dim, &la, &ha) || !k6_fp32_exact(b, nb, dim, &lb, &hb)) return false;
+  const double span = (double)std::max(ha, hb) - (double)std::min(la, lb);
+  return span * span * (double)dim < 16777216.0;
+}
+
 }  // namespace
 
 struct dvsg_ctx {
@@ -248,6 +273,8 @@ struct dvsg_ctx {
   int timing_pending = 0;  // 1: search only, 2: pipeline
   std::atomic<uint64_t> launches{0};
   int assign_path = -1;  // K5 variant of the last context assign (launch_assign's *path)
+  int knn_exact = -1;          // last build_graph / brute_force_topk: 0 fp32 tiles, 1 exact mode
+  uint64_t knn_fallbacks = 0;  // exact mode: rows the certificate sent to the fp64 scan
 };
 
 namespace {
@@ -1894,8 +1921,22 @@ dvsg_status dvsg_build_graph(dvsg_ctx* c, const float* vectors, uint64_t n, int 
     cuda_check(cudaMemset(dv.p, 0, n * (uint64_t)dpad * 4), "memset");
     cuda_check(cudaMemcpy2D(dv.p, (size_t)dpad * 4, vectors, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "H2D");
     legacy_fence();
-    cuda_check(dvsg::launch_knn_build(dv.p, n, dim, dpad, out_degree, da.p, c->stream), "knn build");
-    c->launches += 1;
+    if (k6_fp32_exact(vectors, n, dim)) {
+      cuda_check(dvsg::launch_knn_build(dv.p, n, dim, dpad, out_degree, da.p, c->stream), "knn build");
+      c->launches += 1;
+      c->knn_exact = 0;
+    } else {  // float data: fp32 candidates + fp64 re-rank + certificate + fp64 fallback
+      DevBuf<unsigned char> ks;
+      ks.reserve(dvsg::knn_exact_scratch_bytes(n), c->stream);
+      cuda_check(dvsg::launch_knn_exact(dv.p, n, dv.p, n, dim, dpad, out_degree, true, da.p, nullptr, ks.p,
+                                        c->stream), "knn build (exact)");
+      c->launches += 3;
+      uint32_t fb = 0;
+      cuda_check(cudaMemcpyAsync(&fb, ks.p, 4, cudaMemcpyDeviceToHost, c->stream), "fallbacks");
+      cuda_check(cudaStreamSynchronize(c->stream), "knn build");
+      c->knn_exact = 1;
+      c->knn_fallbacks = fb;
+    }
     cuda_check(cudaStreamSynchronize(c->stream), "knn build");
     cuda_check(cudaMemcpy(adjacency_out, da.p, n * (uint64_t)out_degree * 4, cudaMemcpyDeviceToHost), "D2H");
   });
@@ -1923,8 +1964,22 @@ dvsg_status dvsg_brute_force_topk(dvsg_ctx* c, const float* db, uint64_t n, int 
     cuda_check(cudaMemcpy2D(dd.p, (size_t)dpad * 4, db, (size_t)dim * 4, (size_t)dim * 4, n, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy2D(dq.p, (size_t)dpad * 4, queries, (size_t)dim * 4, (size_t)dim * 4, nq, cudaMemcpyHostToDevice), "H2D");
     legacy_fence();
-    cuda_check(dvsg::launch_brute_force(dq.p, nq, dd.p, n, dpad, k, oi.p, od.p, c->stream), "brute force");
-    c->launches += 1;
+    if (k6_fp32_exact2(db, n, queries, nq, dim)) {
+      cuda_check(dvsg::launch_brute_force(dq.p, nq, dd.p, n, dpad, k, oi.p, od.p, c->stream), "brute force");
+      c->launches += 1;
+      c->knn_exact = 0;
+    } else {
+      DevBuf<unsigned char> ks;
+      ks.reserve(dvsg::knn_exact_scratch_bytes(nq), c->stream);
+      cuda_check(dvsg::launch_knn_exact(dq.p, nq, dd.p, n, dim, dpad, k, false, oi.p, od.p, ks.p, c->stream),
+                 "brute force (exact)");
+      c->launches += 3;
+      uint32_t fb = 0;
+      cuda_check(cudaMemcpyAsync(&fb, ks.p, 4, cudaMemcpyDeviceToHost, c->stream), "fallbacks");
+      cuda_check(cudaStreamSynchronize(c->stream), "brute force");
+      c->knn_exact = 1;
+      c->knn_fallbacks = fb;
+    }
     cuda_check(cudaStreamSynchronize(c->stream), "brute force");
     cuda_check(cudaMemcpy(out_ids, oi.p, nq * (uint64_t)k * 4, cudaMemcpyDeviceToHost), "D2H");
     cuda_check(cudaMemcpy(out_dists, od.p, nq * (uint64_t)k * 4, cudaMemcpyDeviceToHost), "D2H");
@@ -2661,6 +2716,13 @@ dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, f
 }
 
 uint64_t dvsg_kernel_launches(dvsg_ctx* c) { return c ? c->launches.load() : 0; }
+
+dvsg_status dvsg_last_knn_info(dvsg_ctx* c, int* exact_mode, uint64_t* fallbacks) {
+  return guarded([&] {
+    if (exact_mode) *exact_mode = c->knn_exact;
+    if (fallbacks) *fallbacks = c->knn_exact == 1 ? c->knn_fallbacks : 0;
+  });
+}
 
 dvsg_status dvsg_last_assign_info(dvsg_ctx* c, int* path, uint64_t* fallbacks) {
   return guarded([&] {

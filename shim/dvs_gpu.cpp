@@ -7,8 +7,9 @@
 //
 //   validate(SearchParams)   graph_index.cpp:14-19      host check (same message)
 //   compute_entry_order      graph_index.cpp:21-44      dvsg_compute_entry_order
-//   build_graph              graph_index.cpp:46-103     dvsg_build_graph (GPU K6) on integer data with
-//                                                       degree <= 32 (exact there); else exact host rows
+//   build_graph              graph_index.cpp:46-103     dvsg_build_graph (GPU K6; fp32 tiles on byte-like
+//                                                       data, fp64 re-rank + certificate otherwise: exact on
+//                                                       any data) for degree <= 32; else exact host rows
 //   beam_search_stats        graph_index.cpp:105-187    dvsg_load_partition + dvsg_beam_search (K1)
 //   beam_search / visited_count  :189-197               via beam_search_stats
 #include <algorithm>
@@ -114,18 +115,7 @@ Backend& backend() {
 
 namespace {
 
-// K6 (dvsg_build_graph) accumulates in fp32: bit-identical to the reference's
-// fp64 squared_l2 only when every sum is an exact fp32 integer.
-bool integer_valued(const dvs::Dataset& d) {
-  double mx = 0.0;
-  for (const float x : d.data) {
-    if (x != std::nearbyint(x)) return false;
-    mx = std::max(mx, (double)std::fabs(x));
-  }
-  return 4.0 * mx * mx * (double)d.dim < 16777216.0;  // every (x - y)^2 partial sum < 2^24
-}
-
-// Exact rows on the host for float data or out_degree > 32 (the K6 limits):
+// Exact rows on the host for out_degree > 32 (the K6 list width):
 // row v = the out_degree smallest (squared_l2, id) keys over u != v, short
 // lists repeated cyclically, a lone node padded with itself
 // (graph_index.cpp:46-97).  O(n^2) like the reference; this shim only serves
@@ -192,8 +182,8 @@ GraphIndex build_graph(const Dataset& partition, std::vector<std::uint32_t> glob
   g.global_ids = std::move(global_ids);
   g.out_degree = out_degree;
   g.adjacency.resize(n * static_cast<std::size_t>(out_degree));
-  if (out_degree <= 32 && integer_valued(partition)) {
-    // K6's fp32 sums are exact here, i.e. equal to the fp64-then-round squared_l2
+  if (out_degree <= 32) {
+    // bit-identical to the fp64-then-round squared_l2 rows on any data (K6 exact mode)
     Backend& b = backend();
     std::lock_guard<std::mutex> lk(b.mu);
     check(dvsg_build_graph(b.get(), partition.data.data(), n, partition.dim, out_degree,

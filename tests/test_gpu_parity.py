@@ -245,6 +245,54 @@ def test_build_graph_matches_reference(ctx, oracle, n, dim, dg):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("n,dim,dg", [(3000, 37, 32), (2500, 96, 16), (700, 128, 24), (5, 7, 8), (1, 3, 3),
+                                      (33, 5, 32)])
+def test_build_graph_float_data_exact(ctx, ref, oracle, n, dim, dg):
+    """K6 exact mode (fp32 candidates + fp64 re-rank + certificate + fp64
+    fallback): rows bit-identical to the compiled reference's build_graph on
+    float data, incl. tiny partitions (cyclic rows) and a lone node."""
+    rng = np.random.default_rng(n + dim)
+    v = rng.normal(size=(n, dim)).astype(np.float32)
+    _, want, _ = ref.build_graph(v, dg)
+    got = ctx.build_graph(v, dg)
+    assert ctx.last_knn_info()[0] == 1
+    assert np.array_equal(got, want), np.argwhere(np.any(got != want, axis=1))[:5]
+    assert np.array_equal(got, oracle.build_graph(v, dg))
+
+
+def test_build_graph_float_ties_and_fallback(ctx, ref):
+    """Exact ties (duplicated rows) and near-ties (points on a sphere around a
+    centre row: distances equal up to rounding) that the certificate must
+    hand to the fp64 fallback; rows still equal the reference's."""
+    rng = np.random.default_rng(9)
+    v = rng.normal(size=(1500, 24)).astype(np.float32)
+    v[100:120] = v[7]
+    ring = rng.normal(size=(60, 24))
+    ring = ring / np.linalg.norm(ring, axis=1, keepdims=True) * 0.5
+    v[200] = 0.0
+    v[201:261] = ring.astype(np.float32)
+    for dg in (8, 32):
+        _, want, _ = ref.build_graph(v, dg)
+        assert np.array_equal(ctx.build_graph(v, dg), want), dg
+        mode, fb = ctx.last_knn_info()
+        assert mode == 1 and fb >= 1, (mode, fb)  # the sphere centre went to the fp64 scan
+
+
+def test_brute_force_float_data_exact(ctx, ref):
+    """brute_force_topk (topk.cpp:12-30) on float data, k = 10 and 32: ids and
+    fp32 distances bit-identical to the reference, incl. duplicated rows."""
+    rng = np.random.default_rng(4)
+    v = rng.normal(size=(20000, 64)).astype(np.float32)
+    v[500:510] = v[3]
+    q = rng.normal(size=(300, 64)).astype(np.float32)
+    q[0] = v[3]
+    for k in (10, 32):
+        wi, wd = ref.brute_force_topk(v, q, k)
+        gi, gd = ctx.brute_force_topk(v, q, k)
+        assert ctx.last_knn_info()[0] == 1
+        assert np.array_equal(gi, wi) and np.array_equal(gd, wd), k
+
+
 def test_build_graph_golden(ctx, golden):
     g = golden("g2_siftlike.npz")
     assert np.array_equal(ctx.build_graph(g["vectors"], 32), g["adjacency"])
