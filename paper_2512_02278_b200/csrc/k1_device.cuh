@@ -3,6 +3,7 @@
 // unit (internal linkage), not a public header.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "dvsg_internal.h"
@@ -321,6 +322,42 @@ __device__ __forceinline__ F2 shfl_xor(F2 v, int off) {
 __device__ __forceinline__ float acc_to_f32(float v) { return v; }
 __device__ __forceinline__ float acc_to_f32(double v) { return (float)v; }
 __device__ __forceinline__ float acc_to_f32(F2 v) { return __fadd_rn(v.hi, v.lo); }
+
+// f64 mode, squared L2: exact by construction.  The lanes add the same fp64
+// terms ((double)x - (double)q)^2 as squared_l2 (distance.cpp:19-27), in a tree
+// instead of i = 0..d-1; both sums lie within (d-1) 2^-53 S of the exact sum of
+// those terms (all >= 0), so the two differ by at most e = (2d+2) 2^-53 tot.
+// If [tot - e, tot + e] holds no f32 rounding midpoint, both round to the same
+// float; otherwise (about one distance in 10^6-10^7) one lane redoes the sum in
+// the reference's order from the row and the query in memory.
+__device__ __noinline__ float l2_f64_sequential(const float* __restrict__ row, const float* __restrict__ qrow,
+                                                int dim) {
+  double s = 0.0;
+  for (int i = 0; i < dim; ++i) {
+    const double t = __dsub_rn((double)row[i], (double)qrow[i]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return (float)s;
+}
+__device__ __forceinline__ float l2_f64_exact(double tot, const float* row, const float* qrow, int dim) {
+  const float f = (float)tot;
+  const double fd = (double)f;
+  const double up = (double)__uint_as_float(__float_as_uint(f) + 1u);  // next float up (f >= 0)
+  const double dn = f > 0.f ? (double)__uint_as_float(__float_as_uint(f) - 1u) : -1.0;
+  const double e = (double)(2 * dim + 2) * 0x1p-53 * tot;
+  if (tot + e < 0.5 * (fd + up) && tot - e > 0.5 * (fd + dn)) return f;
+  return l2_f64_sequential(row, qrow, dim);
+}
+// key distance of a finished accumulator (the one rounding point of every mode)
+template <typename ACC, int METRIC>
+__device__ __forceinline__ float finish_dist(const ACC& tot, const float* row, const float* qrow, int dim) {
+  if constexpr (std::is_same<ACC, double>::value && METRIC == 0) {
+    return l2_f64_exact(tot, row, qrow, dim);
+  } else {
+    (void)row; (void)qrow; (void)dim;
+    return METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
+  }
+}
 
 // U partial sums per lane -> lane holds the full sum of vector
 // (lane >> (5 - log2 U)) & (U - 1): log2(U) "transpose" stages that halve the

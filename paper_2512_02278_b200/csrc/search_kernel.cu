@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MIN
           bool pass = false;
           uint64_t mykey = 0;
           if ((lane & ((32 >> LU) - 1)) == 0 && ci < M) {
-            const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
+            const float dist = finish_dist<ACC, METRIC>(tot, vbase + (uint64_t)cand[ci] * rstride,
+                                                        a.queries + (uint64_t)qi * (uint64_t)a.dim, a.dim);
             mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
             pass = mykey < thresh;
           }

@@ -60,8 +60,8 @@ struct ShardState {
 // sink(valid, ci, key) is called by every lane (warp-collective).
 template <int VPL, typename ACC, int METRIC, typename Sink>
 __device__ __forceinline__ void score_ids(const uint32_t* cand, int M, const float4 (&q)[VPL],
-                                          const float* vloc, uint32_t lo, int dpad, int lane,
-                                          int warp, Sink&& sink) {
+                                          const float* qrow, int dim, const float* vloc, uint32_t lo,
+                                          int dpad, int lane, int warp, Sink&& sink) {
   constexpr int U = VPL >= 8 ? 1 : (8 / VPL);
   constexpr int LU = ilog2(U);
   for (int cb = warp * U; cb < M; cb += kWarps * U) {
@@ -102,7 +102,7 @@ __device__ __forceinline__ void score_ids(const uint32_t* cand, int M, const flo
     const bool valid = (lane & ((32 >> LU) - 1)) == 0 && ci < M;
     uint64_t key = 0;
     if (valid) {
-      const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
+      const float dist = finish_dist<ACC, METRIC>(tot, vloc + (uint64_t)(cand[ci] - lo) * (uint64_t)dpad, qrow, dim);
       key = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
     }
     sink(valid, ci, key);
@@ -146,7 +146,7 @@ __device__ void serve_request(const ShardArgs& sh, int me, int job, uint32_t* ca
   __syncthreads();
   unsigned char* rb = sh.views[o].reply + ((size_t)c * sh.nranks + me) * sh.reply_stride;
   uint64_t* keys = reinterpret_cast<uint64_t*>(rb + 16);
-  score_ids<VPL, ACC, METRIC>(cand, cnt, qs, mine.vec, lo, dpad, lane, warp,
+  score_ids<VPL, ACC, METRIC>(cand, cnt, qs, qsrc, dim, mine.vec, lo, dpad, lane, warp,
                               [&](bool valid, int ci, uint64_t key) {
                                 if (valid) keys[ci] = key;  // NVLink peer store
                               });
@@ -372,7 +372,8 @@ __global__ void __launch_bounds__(kThreads, 4)
         }
 
         // ---- score own-shard candidates (as K1)
-        score_ids<VPL, ACC, METRIC>(cand, M, q, mine.vec, lo, a.dpad, lane, warp,
+        score_ids<VPL, ACC, METRIC>(cand, M, q, a.queries + (uint64_t)qi * (uint64_t)a.dim, a.dim, mine.vec, lo,
+                                    a.dpad, lane, warp,
                                     [&](bool valid, int, uint64_t key) {
                                       const bool pass = valid && key < thresh;
                                       const unsigned b = __ballot_sync(full, pass);

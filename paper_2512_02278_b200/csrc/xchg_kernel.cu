@@ -506,8 +506,11 @@ __device__ __forceinline__ void score_warp_block(const XgArgs& a, const ScoreTab
       const ACC tot = transpose_reduce<U, ACC>(part, lane);
       if ((lane & ((32 >> LU) - 1)) == 0) {
         const int e = round * U + ((lane >> (5 - LU)) & (U - 1));
-        const float dist = METRIC == 0 ? acc_to_f32(tot) : -acc_to_f32(tot);
-        wk[e] = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)(uint32_t)wq[e] << 1);
+        const uint64_t req = wq[e];
+        const float dist = finish_dist<ACC, METRIC>(
+            tot, lbase - lane * 4 + (uint64_t)((uint32_t)req - lo) * (uint32_t)a.dpad,
+            qbase + (uint64_t)(uint32_t)(req >> 32) * (uint32_t)a.dpad, a.dim);
+        wk[e] = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)(uint32_t)req << 1);
       }
     }
     __syncwarp();
