@@ -348,10 +348,13 @@ __device__ __forceinline__ float l2_f64_exact(double tot, const float* row, cons
   if (tot + e < 0.5 * (fd + up) && tot - e > 0.5 * (fd + dn)) return f;
   return l2_f64_sequential(row, qrow, dim);
 }
+#ifndef DVSG_F64_GUARD
+#define DVSG_F64_GUARD 1  // 0: round the tree sum unconditionally (A/B of the guard only)
+#endif
 // key distance of a finished accumulator (the one rounding point of every mode)
 template <typename ACC, int METRIC>
 __device__ __forceinline__ float finish_dist(const ACC& tot, const float* row, const float* qrow, int dim) {
-  if constexpr (std::is_same<ACC, double>::value && METRIC == 0) {
+  if constexpr (std::is_same<ACC, double>::value && METRIC == 0 && DVSG_F64_GUARD) {
     return l2_f64_exact(tot, row, qrow, dim);
   } else {
     (void)row; (void)qrow; (void)dim;

@@ -582,10 +582,9 @@ def test_cfg4_shape_ip768_k100_beam256(ctx, oracle):
 @pytest.mark.parametrize("metric", ["l2", "ip"])
 def test_f64_float_data_10k_queries_768d(ctx, oracle, metric):
     """The f64 mode on float data at scale: 10k queries at 768-d against the
-    oracle's sequential fp64 (distance.cpp:19-27 order).  The kernel sums lane
-    partials through a tree, so bit identity is observed, not guaranteed; the
-    bar is north_star's (>= 99.9% identical id lists, 1e-4 relative) and the
-    test reports how many lists / distances actually differ."""
+    oracle's sequential fp64 (distance.cpp:19-27 order).  L2 is exact by
+    construction (finish_dist) and must match every row; inner product (no
+    reference) keeps north_star's bar (>= 99.9% identical id lists, 1e-4)."""
     n, dim, nq = 20000, 768, 10000
     rng = np.random.default_rng(8)
     basis = rng.normal(size=(32, dim)).astype(np.float32)
@@ -608,6 +607,30 @@ def test_f64_float_data_10k_queries_768d(ctx, oracle, metric):
     vis_same = int(np.sum(got[3] == want[3]))
     print(f"  visited counters equal on {vis_same}/{nq} queries")
     assert vis_same >= int(np.ceil(0.999 * nq))
+    if metric == "l2":  # exact by construction (finish_dist): every row, every distance
+        assert same == nq and dist_same == nq and vis_same == nq
+
+
+def test_f64_tree_sum_rounding_boundary(ctx, oracle):
+    """A distance whose tree-ordered fp64 sum and the reference's sequential
+    sum round to different floats: terms 1, 2^-24 (lane 0) and four 2^-54
+    (lane 1).  Sequentially each 2^-54 is absorbed and the sum stays at the
+    midpoint 1 + 2^-24 (-> 1.0, ties to even); the tree adds 2^-52 at once and
+    lands above it (-> 1 + 2^-23).  finish_dist must detect the boundary and
+    return the reference's 1.0."""
+    rng = np.random.default_rng(3)
+    v = (3.0 + rng.random((40, 8))).astype(np.float32)
+    v[0] = np.array([1.0, 2.0 ** -12, 0, 0, 2.0 ** -27, 2.0 ** -27, 2.0 ** -27, 2.0 ** -27], np.float32)
+    q = np.zeros((2, 8), np.float32)
+    q[1, 1] = 2.0 ** -12  # a second boundary case: 1 + 4 x 2^-54 sequential -> 1.0
+    adj = oracle.build_graph(v, 8)
+    eo = oracle.compute_entry_order(v)
+    gids = np.arange(len(v), dtype=np.uint32)
+    # entry_count = n: every row is scored in the entry phase
+    want = oracle.beam_search(v, gids, adj, eo, q, 1, 8, 5, len(v), metric=0)
+    got = _search(ctx, v, adj, q, dvs.SearchParams(1, 8, 5, len(v), accum="f64"), eo=eo)
+    assert want[1][0, 0] == np.float32(1.0) and want[0][0, 0] == 0
+    _assert_same(got, want, True, "f64 boundary")
 
 
 def test_cfg3_shape_d96_beam_sweep(ctx, oracle):
