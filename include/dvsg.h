@@ -45,9 +45,11 @@ typedef int dvsg_status;
 #define DVSG_METRIC_L2 0 /* squared_l2, distance.cpp:19-27 */
 #define DVSG_METRIC_IP 1 /* -dot (distance.cpp:35-42); extension, parity unpinned */
 
-#define DVSG_ACCUM_F64 0 /* fp64 lane partials + fp64 tree, rounded once to f32 (parity mode) */
+#define DVSG_ACCUM_F64 0 /* fp64 lane partials + fp64 tree, rounded once to f32 (parity mode; L2:
+                          a distance near an f32 rounding boundary is redone in distance.cpp's
+                          sequential order, so every key equals squared_l2's) */
 #define DVSG_ACCUM_F32 1 /* fp32 lane partials + fp32 tree (fast mode); exact on integer-valued
-                          data, upgraded to F32C / F64 on anything else (dvsg_index_integral) */
+                          data, upgraded to F64 (L2) / F32C (IP) on anything else (dvsg_index_integral) */
 #define DVSG_ACCUM_F32C 2 /* compensated fp32 (TwoSum / FMA TwoProd pairs): ~48-bit sums */
 
 typedef struct dvsg_ctx dvsg_ctx;

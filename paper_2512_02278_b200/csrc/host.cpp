@@ -373,8 +373,10 @@ void validate_params(const dvsg_search_params* p) {
 dvsg_search_params effective_params(const dvsg_ctx* c, const dvsg_search_params* p) {
   dvsg_search_params e = *p;
   static const bool allow = env_u64("DVSG_ALLOW_F32_FLOAT", 0) != 0;
+  // L2 -> f64 (exact by construction, finish_dist; with the wide-row K1 it is
+  // also the faster mode at 768-d), inner product -> f32c (no reference to match)
   if (e.accum == DVSG_ACCUM_F32 && !c->all_integral && !allow)
-    e.accum = (e.metric == DVSG_METRIC_IP || c->dim >= 384) ? DVSG_ACCUM_F32C : DVSG_ACCUM_F64;
+    e.accum = e.metric == DVSG_METRIC_IP ? DVSG_ACCUM_F32C : DVSG_ACCUM_F64;
   return e;
 }
 
