@@ -273,6 +273,7 @@ struct dvsg_ctx {
   int timing_pending = 0;  // 1: search only, 2: pipeline
   std::atomic<uint64_t> launches{0};
   int assign_path = -1;  // K5 variant of the last context assign (launch_assign's *path)
+  bool pipeline_pageable = false;  // last dvsg_run_pipeline saw pageable host buffers
   int knn_exact = -1;          // last build_graph / brute_force_topk: 0 fp32 tiles, 1 exact mode
   uint64_t knn_fallbacks = 0;  // exact mode: rows the certificate sent to the fp64 scan
 };
@@ -1844,9 +1845,7 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
     cudaEvent_t* tv = c->tl_ev + 1;
     c->tl_mb = tl ? (int)mb : 0;
     if (tl) cuda_check(cudaEventRecord(c->tl_ev[0], xs), "event");
-    // every H2D first: a D2H queued on the copy stream waits for its batch's
-    // compute, so an H2D queued behind it would serialize the whole pipeline
-    for (uint64_t i = 0; i < mb; ++i) {
+    auto h2d = [&](uint64_t i) {
       const uint64_t q0 = edge(i), n_i = edge(i + 1) - q0;
       if (tl) cuda_check(cudaEventRecord(tv[6 * i + 0], xs), "event");
       if (n_i)
@@ -1854,33 +1853,79 @@ dvsg_status dvsg_run_pipeline(dvsg_ctx* c, const float* queries, uint64_t nq, in
                                    n_i * (uint64_t)dim * 4, cudaMemcpyHostToDevice, xs), "H2D");
       if (tl) cuda_check(cudaEventRecord(tv[6 * i + 1], xs), "event");
       cuda_check(cudaEventRecord(evh[i], xs), "event");
-    }
-    for (uint64_t i = 0; i < mb; ++i) {
-      const uint64_t q0 = edge(i), q1 = edge(i + 1), n_i = q1 - q0;
+    };
+    auto compute = [&](uint64_t i) {
+      const uint64_t q0 = edge(i), n_i = edge(i + 1) - q0;
       if (n_i == 0) {
-        if (tl)
-          for (int e = 2; e < 6; ++e) cuda_check(cudaEventRecord(tv[6 * i + e], xs), "event");
-        continue;
+        if (tl) {
+          cuda_check(cudaEventRecord(tv[6 * i + 2], cs), "event");
+          cuda_check(cudaEventRecord(tv[6 * i + 3], cs), "event");
+        }
+        return;
       }
       float* dq = c->io_f.p + q0 * (uint64_t)dim;
       cuda_check(cudaStreamWaitEvent(cs, evh[i], 0), "wait");
       if (tl) cuda_check(cudaEventRecord(tv[6 * i + 2], cs), "event");
       cuda_check(dvsg::launch_check_finite(dq, n_i * (uint64_t)dim, c->err_flag.p, cs), "finite check");
       c->launches += 1;
-      uint32_t* ids_i = c->io_u.p + q0 * k;
-      uint32_t* cnt_i = c->io_u.p + nq * k + q0;
-      float* d_i = od.p + q0 * k;
-      float* v_i = out_vectors ? ov.p + q0 * k * (uint64_t)dim : nullptr;
-      pipeline_device(c, dq, n_i, dim, p, fanout, ids_i, d_i, cnt_i, v_i, c->u_visited.p + q0 * (uint64_t)fanout, false);
+      pipeline_device(c, dq, n_i, dim, p, fanout, c->io_u.p + q0 * k, od.p + q0 * k, c->io_u.p + nq * k + q0,
+                      out_vectors ? ov.p + q0 * k * (uint64_t)dim : nullptr, c->u_visited.p + q0 * (uint64_t)fanout,
+                      false);
       if (tl) cuda_check(cudaEventRecord(tv[6 * i + 3], cs), "event");
       cuda_check(cudaEventRecord(evc[i], cs), "event");
+    };
+    auto d2h = [&](uint64_t i) {
+      const uint64_t q0 = edge(i), n_i = edge(i + 1) - q0;
+      if (n_i == 0) {
+        if (tl) {
+          cuda_check(cudaEventRecord(tv[6 * i + 4], xs), "event");
+          cuda_check(cudaEventRecord(tv[6 * i + 5], xs), "event");
+        }
+        return;
+      }
       cuda_check(cudaStreamWaitEvent(xs, evc[i], 0), "wait");
       if (tl) cuda_check(cudaEventRecord(tv[6 * i + 4], xs), "event");
-      cuda_check(cudaMemcpyAsync(out_ids + q0 * k, ids_i, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
-      cuda_check(cudaMemcpyAsync(out_dists + q0 * k, d_i, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
-      cuda_check(cudaMemcpyAsync(out_count + q0, cnt_i, n_i * 4, cudaMemcpyDeviceToHost, xs), "D2H");
-      if (out_vectors) cuda_check(cudaMemcpyAsync(out_vectors + q0 * k * (uint64_t)dim, v_i, n_i * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      cuda_check(cudaMemcpyAsync(out_ids + q0 * k, c->io_u.p + q0 * k, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      cuda_check(cudaMemcpyAsync(out_dists + q0 * k, od.p + q0 * k, n_i * k * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      cuda_check(cudaMemcpyAsync(out_count + q0, c->io_u.p + nq * k + q0, n_i * 4, cudaMemcpyDeviceToHost, xs), "D2H");
+      if (out_vectors)
+        cuda_check(cudaMemcpyAsync(out_vectors + q0 * k * (uint64_t)dim, ov.p + q0 * k * (uint64_t)dim,
+                                   n_i * k * (uint64_t)dim * 4, cudaMemcpyDeviceToHost, xs), "D2H");
       if (tl) cuda_check(cudaEventRecord(tv[6 * i + 5], xs), "event");
+    };
+    // Pageable host buffers make cudaMemcpyAsync host-synchronous: a D2H
+    // returns only after its batch's compute and copy, so issued right after
+    // that compute it would keep the host from queueing the next batch and
+    // leave the GPU idle between microbatches.  Then the order is H2D(0),
+    // C(0), H2D(1), C(1), D2H(0), H2D(2), C(2), D2H(1), ...: while the host
+    // stages one copy the GPU already holds the next compute.
+    auto pinned = [](const void* ptr) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+    };
+    const bool pageable = !pinned(queries) || !pinned(out_ids) || !pinned(out_dists) || !pinned(out_count) ||
+                          (out_vectors && !pinned(out_vectors));
+    c->pipeline_pageable = pageable;
+    if (!pageable) {
+      // every H2D first: a D2H queued on the copy stream waits for its batch's
+      // compute, so an H2D queued behind it would serialize the whole pipeline
+      for (uint64_t i = 0; i < mb; ++i) h2d(i);
+      for (uint64_t i = 0; i < mb; ++i) {
+        compute(i);
+        d2h(i);
+      }
+    } else {
+      h2d(0);
+      for (uint64_t i = 0; i < mb; ++i) {
+        compute(i);
+        if (i + 1 < mb) h2d(i + 1);
+        if (i >= 1) d2h(i - 1);
+      }
+      d2h(mb - 1);
     }
     cuda_check(dvsg::launch_reduce_u64(c->u_visited.p, nq * (uint64_t)fanout, reinterpret_cast<unsigned long long*>(c->io_u64.p), cs), "reduce");
     c->launches += 1;
