@@ -4,6 +4,23 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Race stress build (-DDVSG_STRESS=1; scripts/stress_check.sh): after every
+// block / warp barrier a pseudo-random 1/8 of the threads sleep up to ~4 us,
+// so code that relies on timing instead of a barrier (a missing
+// __syncthreads / __syncwarp, a read racing a write) sees its other
+// interleavings.  compute-sanitizer is not available on this pool; the parity
+// suite run against this build is the substitute.  Never in release builds.
+#if defined(__CUDACC__) && defined(DVSG_STRESS) && DVSG_STRESS
+__device__ __forceinline__ void dvsg_jitter() {
+  unsigned t = (unsigned)clock() * 2654435761u ^ (threadIdx.x * 40503u) ^ (blockIdx.x * 9973u);
+  t ^= t >> 15;
+  t *= 2246822519u;
+  if ((t >> 29) == 0) __nanosleep((t >> 6) & 4095u);
+}
+#define __syncthreads() (__syncthreads(), dvsg_jitter())
+#define __syncwarp(...) (__syncwarp(__VA_ARGS__), dvsg_jitter())
+#endif
+
 namespace dvsg {
 
 #ifndef DVSG_K1_THREADS
