@@ -33,6 +33,7 @@
 // LBO = 128 (the 16-byte K chunks of one 8-row core matrix are adjacent) and
 // SBO = K/8 * 128 (8-row groups follow each other).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "dvsg_internal.h"
@@ -96,16 +97,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "=r"(r[30]), "=r"(r[31])                                                                             \
       : "r"(taddr))
 
-// dynamic smem per CTA: A (128 x K) + 2 x B (128 x K) + survivor buffer + barrier
-__host__ __device__ inline size_t tc_smem_bytes(int row_bytes) {
-  return (size_t)3 * TCM * row_bytes + (size_t)32 * TCM * 8 + 64;
+// dynamic smem per CTA: A (128 x K) + 2 x B (128 x K) + a survivor buffer per
+// epilogue group + barrier
+__host__ __device__ inline size_t tc_smem_bytes(int row_bytes, int groups = 1) {
+  return (size_t)3 * TCM * row_bytes + (size_t)groups * 32 * TCM * 8 + 64;
 }
 
 // T = uint16_t: bf16 operands (kind::f16, K = 16 per MMA); T = float: tf32
 // operands read from fp32 storage (kind::tf32, K = 8 per MMA).  Either way one
 // MMA consumes a 32-byte K slice of every row.
-template <typename T>
-__global__ void __launch_bounds__(128, 1)
+// G epilogue groups of 4 warps: warp w reads TMEM lanes 32*(w%4).. (its 32
+// rows) and group g = w/4 scans columns [g*128/G, (g+1)*128/G) of every tile
+// into its own lists; at the end group 1 hands its lists to group 0, which
+// merges and writes.  G = 2 doubles the warps that hide the epilogue's latency.
+template <typename T, int G>
+__global__ void __launch_bounds__(128 * G, 1)
 range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm,
                      const T* __restrict__ cols, const float* __restrict__ cnorm, int kpad,
                      const uint32_t* __restrict__ row_map, const RangeBlock* __restrict__ blocks,
@@ -118,11 +124,15 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
   const int row_bytes = kpad * (int)sizeof(T);
   auto sb = [&](int b) { return smem + (size_t)(1 + b) * TCM * row_bytes; };  // B double buffer
   __shared__ float cn[2][TCN];  // column norms of the two B tiles (static smem: LDS, not generic loads)
-  uint64_t* cbuf = reinterpret_cast<uint64_t*>(smem + (size_t)3 * TCM * row_bytes);  // [32][128]: survivor j of row t at j*128 + t
-  uint64_t* bar = cbuf + 32 * TCM;
+  // per group [32][128]: survivor j of row t at j*128 + t
+  uint64_t* cbuf0 = reinterpret_cast<uint64_t*>(smem + (size_t)3 * TCM * row_bytes);
+  uint64_t* bar = cbuf0 + G * 32 * TCM;
   __shared__ uint32_t tmem_slot;
 
+  constexpr int NT = 128 * G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = tid >> 7, rt = tid & 127, rw = warp & 3;  // group, row (= TMEM lane), lane quarter
+  uint64_t* cbuf = cbuf0 + grp * 32 * TCM;
   const RangeBlock blk = blocks[blockIdx.x];
   const int nrows = (int)blk.nrows;
   const int kch = row_bytes / 16;  // 16-byte chunks per row
@@ -141,11 +151,11 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
   const uint32_t tmem = tmem_slot;
 
   // ---- this thread's row: physical index, norm; the warp's 32 row lists
-  const bool rvalid = tid < nrows;
-  const uint32_t prow = rvalid ? (row_map ? row_map[blk.row0 + tid] : blk.row0 + tid) : 0u;
+  const bool rvalid = rt < nrows;
+  const uint32_t prow = rvalid ? (row_map ? row_map[blk.row0 + rt] : blk.row0 + rt) : 0u;
   const float nr = rvalid ? rnorm[prow] : 0.f;
-  const uint64_t orow = (flags & 8) ? (uint64_t)prow : (uint64_t)blk.out_row0 + (uint64_t)tid;
-  uint64_t top[32];  // top[rr] at lane i: i-th smallest key of row warp*32 + rr
+  const uint64_t orow = (flags & 8) ? (uint64_t)prow : (uint64_t)blk.out_row0 + (uint64_t)rt;
+  uint64_t top[32];  // top[rr] at lane i: i-th smallest key of row rw*32 + rr (this group's columns)
   // this thread's row: current m-th key -- (+inf, 0) while the list is
   // short, so the padding columns (+inf) never pass
   const uint64_t kInfKey = (uint64_t)f2ord(__int_as_float(0x7F800000)) << 32;
@@ -154,7 +164,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) {
     top[rr] = ~0ull;
-    if (flags & 4) {  // continue from the lists already in the output
+    if ((flags & 4) && grp == 0) {  // continue from the lists already in the output
       const uint64_t o = __shfl_sync(0xFFFFFFFFu, orow, rr);
       const bool v = __shfl_sync(0xFFFFFFFFu, rvalid, rr);
       uint32_t id = 0xFFFFFFFFu;
@@ -172,7 +182,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
   }
 
   // ---- A: the block's rows, canonical K-major layout
-  for (int c = tid; c < TCM * kch; c += 128) {
+  for (int c = tid; c < TCM * kch; c += NT) {
     const int r = c / kch, kc = c - r * kch;
     const uint32_t pr = r < nrows ? (row_map ? row_map[blk.row0 + r] : blk.row0 + r) : 0u;
     cp16(s32(sa + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), rows + (uint64_t)pr * kpad + kc * kEl, r < nrows);
@@ -195,13 +205,13 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
   bool have = next_tile(li, c0);
   auto load_b = [&](int buf, uint32_t l, uint32_t c) {
     const uint32_t end = ranges[l].y;
-    for (int q = tid; q < TCN * kch; q += 128) {
+    for (int q = tid; q < TCN * kch; q += NT) {
       const int r = q / kch, kc = q - r * kch;
       const bool v = c + r < end;
       cp16(s32(sb(buf) + (r >> 3) * sbo + kc * lbo + (r & 7) * 16), cols + (uint64_t)(v ? c + r : 0) * kpad + kc * kEl,
            v);
     }
-    cn[buf][tid] = c + tid < end ? cnorm[c + tid] : __int_as_float(0x7F800000);  // +inf: never a survivor
+    if (tid < TCN) cn[buf][tid] = c + tid < end ? cnorm[c + tid] : __int_as_float(0x7F800000);  // +inf: never a survivor
     cp_commit();
   };
   if (have) load_b(0, li, c0);
@@ -247,11 +257,11 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
     mbar_wait(bar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // ---- epilogue: 128 columns in 4 TMEM loads of 32
+    // ---- epilogue: this group's 128/G columns in TMEM loads of 32
 #pragma unroll 1
-    for (int part = 0; part < TCN / 32; ++part) {
+    for (int part = grp * (4 / G); part < (grp + 1) * (4 / G); ++part) {
       uint32_t r[32];
-      TMEM_LD32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(part * 32), r);
+      TMEM_LD32(tmem + ((uint32_t)(rw * 32) << 16) + (uint32_t)(part * 32), r);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       // (1) this thread's row: survivors of the m-th-key filter -> cbuf
       int ns = 0;
@@ -263,7 +273,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
           const float dist = fmaxf(fmaf(-2.f, __uint_as_float(r[j]), nr + cn[buf][cl]), 0.f);
           const uint64_t key = ((uint64_t)f2ord(dist) << 32) | col;
           const bool ok = key < thr && !((flags & 1) && col == prow);
-          if (ok) cbuf[ns * TCM + tid] = key;
+          if (ok) cbuf[ns * TCM + rt] = key;
           ns += ok ? 1 : 0;
         }
       }
@@ -273,7 +283,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
       for (int rr = 0; rr < 32; ++rr) {
         const int n = __shfl_sync(0xFFFFFFFFu, ns, rr);
         if (n == 0) continue;
-        const int row = warp * 32 + rr;
+        const int row = rw * 32 + rr;
         for (int s2 = 0; s2 < n; ++s2) {
           const uint64_t key = cbuf[s2 * TCM + row];
           const unsigned gt = __ballot_sync(0xFFFFFFFFu, top[rr] > key);
@@ -296,9 +306,35 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
     have = nhave;
   }
 
+  if constexpr (G == 2) {  // group 1's lists -> group 0 (cbuf of group 1 as the hand-over buffer)
+    if (grp == 1) {
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) cbuf[lane * TCM + rw * 32 + rr] = top[rr];
+    }
+    __syncthreads();
+    if (grp == 0) {
+      const uint64_t* other = cbuf0 + 32 * TCM;
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) {
+        const int row = rw * 32 + rr;
+        for (int s2 = 0; s2 < 32; ++s2) {
+          const uint64_t key = other[s2 * TCM + row];
+          if (key == ~0ull) break;  // sorted: the rest are empty
+          const unsigned gt = __ballot_sync(0xFFFFFFFFu, top[rr] > key);
+          if (gt == 0) break;  // sorted: no later key can enter either
+          const int pos = __ffs(gt) - 1;
+          const uint64_t up = __shfl_up_sync(0xFFFFFFFFu, top[rr], 1);
+          if (lane > pos) top[rr] = up;
+          if (lane == pos) top[rr] = key;
+        }
+      }
+    }
+  }
+
   // ---- emit (same rules as range_topk_kernel): lane j writes entry j of each row
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) {
+    if (grp != 0) break;
     if (!__shfl_sync(0xFFFFFFFFu, rvalid, rr)) continue;
     const uint64_t o = __shfl_sync(0xFFFFFFFFu, orow, rr);
     const int nv = __popc(__ballot_sync(0xFFFFFFFFu, lane < m && top[rr] != ~0ull));
@@ -336,24 +372,46 @@ __global__ void to_bf16_kernel(const float* __restrict__ x, uint64_t n, int dpad
 
 size_t range_topk_tc_smem_bytes(int kpad) { return tc_smem_bytes(kpad * 2); }
 
+template <typename T, int G>
+cudaError_t launch_tc_g(const T* rows, const float* rnorm, const T* cols, const float* cnorm, int kpad,
+                        const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks, const uint32_t* list_off,
+                        const uint2* ranges, int m, int flags, uint32_t* out_ids, float* out_dists,
+                        uint64_t out_stride, size_t smem, cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(range_topk_tc_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  for (uint64_t b0 = 0; b0 < nblocks; b0 += 0x7FFFFFFFull) {
+    const uint64_t nb = nblocks - b0 < 0x7FFFFFFFull ? nblocks - b0 : 0x7FFFFFFFull;
+    range_topk_tc_kernel<T, G><<<(unsigned)nb, 128 * G, smem, stream>>>(rows, rnorm, cols, cnorm, kpad, row_map,
+                                                                       blocks + b0, list_off, ranges, m, flags,
+                                                                       out_ids, out_dists, out_stride);
+  }
+  return cudaGetLastError();
+}
+
+// groups: 2 pays a fixed hand-over merge per block and a second list warm-up;
+// it wins on long column lists (large-C assign: 32 tiles per block, 60 -> 51 ms
+// at 1M x 4096) and loses on the graph build's short merged passes (~9 tiles
+// per block: 8.2 -> 20.5 s of kNN at 100M), so each caller picks.
 template <typename T>
 cudaError_t launch_tc_t(const T* rows, const float* rnorm, const T* cols, const float* cnorm, int kpad,
                         const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks, const uint32_t* list_off,
                         const uint2* ranges, int m, int flags, uint32_t* out_ids, float* out_dists,
-                        uint64_t out_stride, cudaStream_t stream) {
+                        uint64_t out_stride, int groups, cudaStream_t stream) {
   const int row_bytes = kpad * (int)sizeof(T);
   if (m < 1 || m > 32 || row_bytes % 32 || kpad < 1 || row_bytes > TCMAXK * 2) return cudaErrorInvalidValue;
   if (nblocks == 0) return cudaSuccess;
-  const size_t smem = tc_smem_bytes(row_bytes);
-  cudaError_t e = cudaFuncSetAttribute(range_topk_tc_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  for (uint64_t b0 = 0; b0 < nblocks; b0 += 0x7FFFFFFFull) {
-    const uint64_t nb = nblocks - b0 < 0x7FFFFFFFull ? nblocks - b0 : 0x7FFFFFFFull;
-    range_topk_tc_kernel<T><<<(unsigned)nb, 128, smem, stream>>>(rows, rnorm, cols, cnorm, kpad, row_map, blocks + b0,
-                                                                 list_off, ranges, m, flags, out_ids, out_dists,
-                                                                 out_stride);
-  }
-  return cudaGetLastError();
+  static const int groups_env = [] {
+    const char* e = std::getenv("DVSG_TC_GROUPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (groups_env > 0) groups = groups_env;
+  // two epilogue groups only if their second survivor buffer fits (227 KB opt-in)
+  if (groups >= 2 && tc_smem_bytes(row_bytes, 2) + 2048 <= 227 * 1024)
+    return launch_tc_g<T, 2>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
+                             out_ids, out_dists, out_stride, tc_smem_bytes(row_bytes, 2), stream);
+  return launch_tc_g<T, 1>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
+                           out_ids, out_dists, out_stride, tc_smem_bytes(row_bytes, 1), stream);
 }
 
 cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const uint16_t* cols, const float* cnorm,
@@ -362,7 +420,7 @@ cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const
                                  float* out_dists, uint64_t out_stride, cudaStream_t stream) {
   if (kpad % 16) return cudaErrorInvalidValue;
   return launch_tc_t<uint16_t>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
-                               out_ids, out_dists, out_stride, stream);
+                               out_ids, out_dists, out_stride, 1, stream);
 }
 
 cudaError_t launch_range_topk_tf32(const float* rows, const float* rnorm, const float* cols, const float* cnorm,
@@ -371,7 +429,7 @@ cudaError_t launch_range_topk_tf32(const float* rows, const float* rnorm, const 
                                    float* out_dists, uint64_t out_stride, cudaStream_t stream) {
   if (kpad % 8) return cudaErrorInvalidValue;
   return launch_tc_t<float>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
-                            out_ids, out_dists, out_stride, stream);
+                            out_ids, out_dists, out_stride, 2, stream);
 }
 
 cudaError_t launch_to_bf16(const float* x, uint64_t n, int dpad, int kpad, uint16_t* out, cudaStream_t stream) {
