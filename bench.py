@@ -659,6 +659,31 @@ def accum_modes(args, torch, dvs, ctx, w, ids_h, cnt_h, dev):
     return out
 
 
+def u8_storage(args, torch, ctx, stream, step, flush, dist, local, b, ids_h, cnt_h, f32_total_ms):
+    """Side measurement (not the headline): the same run_pipeline step with K1
+    gathering a byte copy of the rows (dvsg_set_vector_storage U8; the byte-
+    valued synthetic data converts exactly), same W/K, L2 flush and events.
+    The reference stores fp32, so the headline stays on fp32 rows."""
+    import paper_2512_02278_b200 as dvs
+    try:
+        ctx.set_vector_storage("u8")
+    except dvs.InvalidArgument as ex:
+        return {"value": None, "note": f"not byte-valued data: {ex}"}
+    try:
+        total_ms, k1_ms, vis, exp, units, launches, clocks = timed_steps(args, torch, ctx, stream, step, flush,
+                                                                         dist, local, stats=False)
+        same = bool(np.array_equal(b.ids.cpu().numpy().view(np.uint32), ids_h) and
+                    np.array_equal(b.counts.cpu().numpy().view(np.uint32), cnt_h))
+    finally:
+        ctx.set_vector_storage("f32")
+    return {"value": args.nq * args.steps / (total_ms / 1e3), "unit": "queries/s",
+            "ms_per_step": total_ms / args.steps, "speedup_vs_f32_rows": f32_total_ms / total_ms,
+            "ids_identical_to_headline": same, "bytes_per_row": args.dim,
+            "note": "K1 reads a uint8 copy of the rows (a quarter of the gather bytes); every coordinate of the "
+                    "synthetic data is an integer in [0, 255], so distances are bit-identical; side measurement, "
+                    "the headline reads fp32 rows like the reference"}
+
+
 def cpu_baseline(args, w, ids_h, cnt_h, dists_h):
     nthreads = os.cpu_count() or 1
     t0 = time.time()
@@ -847,6 +872,9 @@ def main():
                                                          dist, world, rank)
     ctx.set_timing(False)
     modes = None if args.no_modes or sharded else accum_modes(args, torch, dvs, ctx, w, ids_h, cnt_h, dev)
+    storage_u8 = None
+    if not args.no_modes and not sharded and args.dim <= 256:
+        storage_u8 = u8_storage(args, torch, ctx, stream, step, flush, dist, local, b, ids_h, cnt_h, total_ms)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -904,6 +932,7 @@ def main():
                      "k1_share_of_step": k1_ms / total_ms if total_ms else None},
         "cpu_baseline": cpu, "e2e": headline["e2e"] if headline else e2e, "gpu_launches": int(headline["gpu_launches"] if headline else launches),
         "accum_modes": modes,
+        "storage_u8": storage_u8,
         "clocks": headline["clocks"] if headline else clocks,
     }
     if world > 1:

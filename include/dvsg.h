@@ -419,6 +419,16 @@ uint64_t dvsg_kernel_launches(dvsg_ctx *ctx);
  * queries whose certificate failed and were finished by the exact kernel).
  * -1 before any assign.  Results are identical on every path. */
 dvsg_status dvsg_last_assign_info(dvsg_ctx *ctx, int *path, uint64_t *fallbacks);
+/* Vector storage K1 reads (whole-graph searches: dvsg_beam_search*,
+ * dvsg_search_units*, dvsg_run_pipeline*).  DVSG_STORAGE_U8 keeps a byte copy
+ * of the resident rows and gathers a quarter of the bytes; results are
+ * bit-identical because every coordinate must be an integer in [0, 255]
+ * (checked here: DVSG_EINVAL otherwise; dim <= 256).  The copy is dropped
+ * automatically when the rows change (call again after loading).  An
+ * extension (the reference stores fp32 only); DVSG_STORAGE_F32 is the default. */
+#define DVSG_STORAGE_F32 0
+#define DVSG_STORAGE_U8 1
+dvsg_status dvsg_set_vector_storage(dvsg_ctx *ctx, int mode);
 /* How the last dvsg_build_graph / dvsg_brute_force_topk of this context ran:
  * *exact_mode 0 = fp32 tiles (byte-like data: every squared distance an exact
  * fp32 integer), 1 = fp32 candidates + fp64 re-rank + certificate (any float

@@ -95,6 +95,7 @@ _SIGS = {
     "dvsg_kernel_launches": (c_uint64, [c_void_p]),
     "dvsg_last_assign_info": (c_int, [c_void_p, c_void_p, c_void_p]),
     "dvsg_last_knn_info": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "dvsg_set_vector_storage": (c_int, [c_void_p, c_int]),
     "dvsg_last_search_stats": (c_int, [c_void_p, P_u64, P_u64, P_u64]),
     "dvsg_debug_counters": (c_int, [c_void_p, c_void_p]),
     "dvsg_row_norms_device": (c_int, [c_void_p, c_void_p, c_uint64, c_int, c_void_p]),

@@ -324,6 +324,14 @@ class Context:
         check(lib.dvsg_last_assign_info(self._h, ctypes.byref(path), ctypes.byref(fb)))
         return int(path.value), int(fb.value)
 
+    def set_vector_storage(self, mode: str) -> None:
+        """"f32" (default) or "u8": K1 gathers a byte copy of the resident rows
+        (every coordinate must be an integer in [0, 255]; results unchanged)."""
+        m = {"f32": 0, "u8": 1}.get(mode)
+        if m is None:
+            raise InvalidArgument(f"set_vector_storage: unknown mode {mode!r}")
+        check(lib.dvsg_set_vector_storage(self._h, m))
+
     def last_knn_info(self):
         """(exact_mode, fallbacks) of the last build_graph / brute_force_topk:
         0 fp32 tiles, 1 fp32 candidates + fp64 re-rank + certificate."""

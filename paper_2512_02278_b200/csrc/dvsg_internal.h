@@ -42,6 +42,7 @@ struct PartDesc {
 
 struct SearchArgs {
   const float* vectors;       // rows x dpad
+  const uint8_t* vectors8;    // nullable: the same rows as bytes (dvsg_set_vector_storage U8; dpad <= 256)
   const uint32_t* adjacency;  // rows x dg
   const uint32_t* gids;       // rows
   const uint32_t* entry;      // rows (per-partition entry order)
@@ -176,6 +177,9 @@ cudaError_t launch_xg_barrier(const XgView* views, int nranks, int me, unsigned 
 // max_grid > 0 caps the persistent grid (one global hash region per CTA).
 cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sms,
                           int max_grid, cudaStream_t stream, int* grid_out);
+// Byte copy of float rows for the U8 vector storage: out[i] = x[i] when every
+// element is an integer in [0, 255]; otherwise bit 0 of *bad is set.
+cudaError_t launch_to_u8(const float* x, uint64_t n, uint8_t* out, int* bad, cudaStream_t stream);
 // Shared-memory bytes K1 needs for these args (hash in smem when hash_global==nullptr).
 size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_smem);
 constexpr int kChunk = 8 * kThreads;  // raw candidates per dedup/score/merge chunk (8 per thread)

@@ -274,6 +274,11 @@ struct dvsg_ctx {
   std::atomic<uint64_t> launches{0};
   int assign_path = -1;  // K5 variant of the last context assign (launch_assign's *path)
   bool pipeline_pageable = false;  // last dvsg_run_pipeline saw pageable host buffers
+  // U8 vector storage (dvsg_set_vector_storage): a byte copy of the resident
+  // rows, valid while vec_gen (bumped on every change of the rows) matches
+  DevBuf<uint8_t> vec8;
+  uint64_t vec_gen = 0, u8_gen = ~0ull;
+  bool want_u8 = false;
   int knn_exact = -1;          // last build_graph / brute_force_topk: 0 fp32 tiles, 1 exact mode
   uint64_t knn_fallbacks = 0;  // exact mode: rows the certificate sent to the fp64 scan
 };
@@ -443,6 +448,7 @@ dvsg::SearchArgs k1_args(dvsg_ctx* c, const dvsg_search_params* p, const K1Shape
                          uint64_t* d_visited) {
   dvsg::SearchArgs a{};
   a.vectors = c->vec.p;
+  a.vectors8 = (c->want_u8 && c->u8_gen == c->vec_gen && !c->sh.active && c->dpad <= 256) ? c->vec8.p : nullptr;
   a.adjacency = c->adj.p;
   a.gids = c->gids.p;
   a.entry = c->entry.p;
@@ -1310,6 +1316,7 @@ dvsg_status dvsg_index_reset(dvsg_ctx* c) {
     c->all_integral = true;
     c->pend = dvsg_ctx::Pending{};
     c->rows = 0;
+    c->vec_gen += 1;
     c->dim = c->dpad = c->dg = 0;
     c->clusters = 0;
     c->sh.active = false;
@@ -1403,6 +1410,7 @@ dvsg_status dvsg_load_partition(dvsg_ctx* c, uint32_t cluster, uint64_t n, int d
     c->part_mono.push_back(ids_increasing(global_ids, n));
     c->all_integral = c->all_integral && integral_all(vectors, n * (uint64_t)dim);
     c->rows = r1;
+    c->vec_gen += 1;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = c->anchors_dirty = true;
   });
 }
@@ -1555,6 +1563,7 @@ dvsg_status dvsg_shard_init(dvsg_ctx* c, int nranks, int rank, uint64_t n_total,
     c->dpad = (dim + 3) & ~3;
     c->dg = out_degree;
     c->rows = n_total;
+    c->vec_gen += 1;
     // own shard rows only (at least one row so the buffer exists)
     const uint64_t rows = std::max<uint64_t>(hi - lo, 1);
     c->vec.reserve(rows * (uint64_t)c->dpad, c->stream);
@@ -1608,6 +1617,7 @@ dvsg_status dvsg_shard_init_resident(dvsg_ctx* c, int nranks, int rank) {
     std::swap(c->vec.cap, own.cap);
     c->parts[0].cluster = 0;
     c->rows = n_total;
+    c->vec_gen += 1;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
     shard_arena_setup(c, nranks, rank, n_total);
   });
@@ -2193,6 +2203,7 @@ dvsg_status dvsg_partition_commit_device(dvsg_ctx* c, int flags) {
     c->part_mono.push_back((flag & 64) == 0);
     c->all_integral = c->all_integral && (flag & 16) == 0;
     c->rows = pd.r0 + pd.n;
+    c->vec_gen += 1;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = c->anchors_dirty = true;
   });
 }
@@ -2764,6 +2775,32 @@ dvsg_status dvsg_last_timings(dvsg_ctx* c, float* search_ms, float* assign_ms, f
 
 uint64_t dvsg_kernel_launches(dvsg_ctx* c) { return c ? c->launches.load() : 0; }
 
+dvsg_status dvsg_set_vector_storage(dvsg_ctx* c, int mode) {
+  return guarded([&] {
+    set_device(c);
+    if (mode == DVSG_STORAGE_F32) {
+      c->want_u8 = false;
+      return;
+    }
+    if (mode != DVSG_STORAGE_U8) fail(DVSG_EINVAL, "set_vector_storage: unknown mode %d", mode);
+    if (c->rows == 0) fail(DVSG_EINVAL, "set_vector_storage: no resident rows");
+    if (c->sh.active) fail(DVSG_EINVAL, "set_vector_storage: U8 serves the whole-graph search only");
+    if (c->dpad > 256) fail(DVSG_EINVAL, "set_vector_storage: U8 needs dim <= 256");
+    const uint64_t n = c->rows * (uint64_t)c->dpad;
+    c->vec8.reserve(n, c->stream);
+    c->err_flag.reserve(1, c->stream);
+    cuda_check(cudaMemsetAsync(c->err_flag.p, 0, sizeof(int), c->stream), "err reset");
+    cuda_check(dvsg::launch_to_u8(c->vec.p, n, c->vec8.p, c->err_flag.p, c->stream), "to u8");
+    c->launches += 1;
+    int bad = 0;
+    cuda_check(cudaMemcpyAsync(&bad, c->err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "flag");
+    cuda_check(cudaStreamSynchronize(c->stream), "to u8");
+    if (bad) fail(DVSG_EINVAL, "set_vector_storage: U8 needs every coordinate to be an integer in [0, 255]");
+    c->want_u8 = true;
+    c->u8_gen = c->vec_gen;
+  });
+}
+
 dvsg_status dvsg_last_knn_info(dvsg_ctx* c, int* exact_mode, uint64_t* fallbacks) {
   return guarded([&] {
     if (exact_mode) *exact_mode = c->knn_exact;
@@ -2907,6 +2944,7 @@ dvsg_status dvsg_load_index_file(dvsg_ctx* c, const char* path, int rank) {
     c->all_integral = true;
     c->pend = dvsg_ctx::Pending{};
     c->rows = 0;
+    c->vec_gen += 1;
     c->dim = c->dpad = c->dg = 0;
     c->parts_dirty = c->slot_dirty = c->locator_dirty = true;
     std::vector<float> v;

@@ -330,7 +330,8 @@ __device__ __forceinline__ float acc_to_f32(F2 v) { return __fadd_rn(v.hi, v.lo)
 // If [tot - e, tot + e] holds no f32 rounding midpoint, both round to the same
 // float; otherwise (about one distance in 10^6-10^7) one lane redoes the sum in
 // the reference's order from the row and the query in memory.
-__device__ __noinline__ float l2_f64_sequential(const float* __restrict__ row, const float* __restrict__ qrow,
+template <typename VT>
+__device__ __noinline__ float l2_f64_sequential(const VT* __restrict__ row, const float* __restrict__ qrow,
                                                 int dim) {
   double s = 0.0;
   for (int i = 0; i < dim; ++i) {
@@ -339,7 +340,8 @@ __device__ __noinline__ float l2_f64_sequential(const float* __restrict__ row, c
   }
   return (float)s;
 }
-__device__ __forceinline__ float l2_f64_exact(double tot, const float* row, const float* qrow, int dim) {
+template <typename VT>
+__device__ __forceinline__ float l2_f64_exact(double tot, const VT* row, const float* qrow, int dim) {
   const float f = (float)tot;
   const double fd = (double)f;
   const double up = (double)__uint_as_float(__float_as_uint(f) + 1u);  // next float up (f >= 0)
@@ -352,8 +354,8 @@ __device__ __forceinline__ float l2_f64_exact(double tot, const float* row, cons
 #define DVSG_F64_GUARD 1  // 0: round the tree sum unconditionally (A/B of the guard only)
 #endif
 // key distance of a finished accumulator (the one rounding point of every mode)
-template <typename ACC, int METRIC>
-__device__ __forceinline__ float finish_dist(const ACC& tot, const float* row, const float* qrow, int dim) {
+template <typename ACC, int METRIC, typename VT = float>
+__device__ __forceinline__ float finish_dist(const ACC& tot, const VT* row, const float* qrow, int dim) {
   if constexpr (std::is_same<ACC, double>::value && METRIC == 0 && DVSG_F64_GUARD) {
     return l2_f64_exact(tot, row, qrow, dim);
   } else {
@@ -477,6 +479,16 @@ __device__ __forceinline__ float4 ldg_f4(const float* p) {
 #else
   return __ldg(reinterpret_cast<const float4*>(p));
 #endif
+}
+
+// 4 byte-stored coordinates (U8 vector storage): raw word, then -> float4 (exact)
+__device__ __forceinline__ uint32_t ldg_u8x4_raw(const uint8_t* p) {
+  uint32_t w;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(w) : "l"(p));
+  return w;
+}
+__device__ __forceinline__ float4 cvt_u8x4(uint32_t w) {
+  return make_float4((float)(w & 0xFFu), (float)((w >> 8) & 0xFFu), (float)((w >> 16) & 0xFFu), (float)(w >> 24));
 }
 
 __device__ __forceinline__ uint32_t ldg_u32_stream(const uint32_t* p) {

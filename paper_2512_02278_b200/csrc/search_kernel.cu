@@ -25,6 +25,7 @@
 //                     truncated at cap (== the reference's sort + resize)
 //   Chunking is exact because top-cap(A u B u C) = top-cap(top-cap(A u B) u C)
 //   for unique keys, and frontier selection only happens between iterations.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -55,10 +56,22 @@ namespace {
 #ifndef DVSG_UVEC_WIDE
 #define DVSG_UVEC_WIDE -1  // vectors in flight per warp at VPL >= 4 (-1: 4, or 2 at VPL 8; 0: DVSG_UVEC / VPL)
 #endif
-template <int VPL, typename ACC, int METRIC, bool FULL>
-__global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MINB) search_kernel(const SearchArgs a) {
+// U8: vectors read from the byte copy (a.vectors8): a quarter of the gather
+// bytes, identical arithmetic (every byte converts exactly to float).
+// Byte rows are a quarter of the bytes but the same latency per row, so they
+// only pay with more rows in flight: a raw 32-bit word per lane and row.
+#ifndef DVSG_UVEC8
+#define DVSG_UVEC8 16
+#endif
+#ifndef DVSG_MINB8
+#define DVSG_MINB8 4
+#endif
+template <int VPL, typename ACC, int METRIC, bool FULL, bool U8>
+__global__ void __launch_bounds__(kThreads, U8 ? DVSG_MINB8 : VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MINB)
+    search_kernel(const SearchArgs a) {
   constexpr int UW = DVSG_UVEC_WIDE < 0 ? (VPL >= 8 ? 2 : 4) : DVSG_UVEC_WIDE;
-  constexpr int U = (VPL >= 4 && UW > 0) ? UW : (VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL));
+  constexpr int U = U8 ? (DVSG_UVEC8 / VPL > 0 ? DVSG_UVEC8 / VPL : 1)
+                       : (VPL >= 4 && UW > 0) ? UW : (VPL >= DVSG_UVEC ? 1 : (DVSG_UVEC / VPL));
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ BlockState st;
 
@@ -90,6 +103,8 @@ __global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MIN
     const uint32_t n = part.n;
     const float* vbase = a.vectors + row0 * (uint64_t)a.dpad;
     const float* lbase = vbase + lane * 4;          // this lane's first dims of row 0
+    const uint8_t* vbase8 = U8 ? a.vectors8 + row0 * (uint64_t)a.dpad : nullptr;
+    const uint8_t* lbase8 = vbase8 + lane * 4;
     const uint32_t* abase = a.adjacency + row0 * (uint64_t)a.dg;
     const uint32_t rstride = (uint32_t)a.dpad;      // u32 x u32 -> u64: one IMAD.WIDE per row
 
@@ -230,24 +245,35 @@ __global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MIN
 #pragma unroll
             for (int u = 0; u < U; ++u) ids_u[u] = cand[cb + u];
           }
-          float4 x[U][VPL];
+          float4 x[U8 ? 1 : U][VPL];
+          uint32_t x8[U8 ? U : 1][VPL];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             // past M: load row 0 (harmless, result discarded by the ci < M test)
             const uint32_t id = cb + u < M ? ids_u[u] : 0u;
-            const float* row = lbase + (uint64_t)id * rstride;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
-              if (FULL || lane * 4 + 128 * v < a.dpad) x[u][v] = ldg_f4(row + 128 * v);
-              else x[u][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+              const bool in = FULL || lane * 4 + 128 * v < a.dpad;
+              if constexpr (U8) {
+                x8[u][v] = in ? ldg_u8x4_raw(lbase8 + (uint64_t)id * rstride + 128 * v) : 0u;
+              } else {
+                x[u][v] = in ? ldg_f4(lbase + (uint64_t)id * rstride + 128 * v) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
             }
           }
           ACC part[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            ACC acc = lane_partial<ACC, METRIC>(x[u][0], q[0]);
+            ACC acc;
+            if constexpr (U8) {
+              acc = lane_partial<ACC, METRIC>(cvt_u8x4(x8[u][0]), q[0]);
 #pragma unroll
-            for (int v = 1; v < VPL; ++v) acc += lane_partial<ACC, METRIC>(x[u][v], q[v]);
+              for (int v = 1; v < VPL; ++v) acc += lane_partial<ACC, METRIC>(cvt_u8x4(x8[u][v]), q[v]);
+            } else {
+              acc = lane_partial<ACC, METRIC>(x[u][0], q[0]);
+#pragma unroll
+              for (int v = 1; v < VPL; ++v) acc += lane_partial<ACC, METRIC>(x[u][v], q[v]);
+            }
             part[u] = acc;
           }
           const ACC tot = transpose_reduce<U, ACC>(part, lane);
@@ -257,8 +283,10 @@ __global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MIN
           bool pass = false;
           uint64_t mykey = 0;
           if ((lane & ((32 >> LU) - 1)) == 0 && ci < M) {
-            const float dist = finish_dist<ACC, METRIC>(tot, vbase + (uint64_t)cand[ci] * rstride,
-                                                        a.queries + (uint64_t)qi * (uint64_t)a.dim, a.dim);
+            const float* qrow = a.queries + (uint64_t)qi * (uint64_t)a.dim;
+            float dist;
+            if constexpr (U8) dist = finish_dist<ACC, METRIC>(tot, vbase8 + (uint64_t)cand[ci] * rstride, qrow, a.dim);
+            else dist = finish_dist<ACC, METRIC>(tot, vbase + (uint64_t)cand[ci] * rstride, qrow, a.dim);
             mykey = ((uint64_t)f2ord(dist) << 32) | ((uint64_t)cand[ci] << 1);
             pass = mykey < thresh;
           }
@@ -326,10 +354,10 @@ __global__ void __launch_bounds__(kThreads, VPL >= 4 ? DVSG_MINB_WIDE : DVSG_MIN
   }
 }
 
-template <int VPL, typename ACC, int METRIC, bool FULL>
+template <int VPL, typename ACC, int METRIC, bool FULL, bool U8 = false>
 cudaError_t launch_t(const SearchArgs& a, int num_sms, int max_grid, cudaStream_t stream,
                      int* grid_out) {
-  auto kern = search_kernel<VPL, ACC, METRIC, FULL>;
+  auto kern = search_kernel<VPL, ACC, METRIC, FULL, U8>;
   const size_t smem = search_smem_bytes(a.cap, a.chp, a.beam, a.hsize, a.hash_global == nullptr);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -346,26 +374,26 @@ cudaError_t launch_t(const SearchArgs& a, int num_sms, int max_grid, cudaStream_
   return cudaGetLastError();
 }
 
-template <int VPL>
+template <int VPL, bool U8>
 cudaError_t launch_v(const SearchArgs& a, int metric, int accum, int num_sms, int mg,
                      cudaStream_t s, int* g) {
   const bool full = a.dpad == 128 * VPL;
   if (accum == 0) {
-    if (metric == 0) return full ? launch_t<VPL, double, 0, true>(a, num_sms, mg, s, g)
-                                 : launch_t<VPL, double, 0, false>(a, num_sms, mg, s, g);
-    return full ? launch_t<VPL, double, 1, true>(a, num_sms, mg, s, g)
-                : launch_t<VPL, double, 1, false>(a, num_sms, mg, s, g);
+    if (metric == 0) return full ? launch_t<VPL, double, 0, true, U8>(a, num_sms, mg, s, g)
+                                 : launch_t<VPL, double, 0, false, U8>(a, num_sms, mg, s, g);
+    return full ? launch_t<VPL, double, 1, true, U8>(a, num_sms, mg, s, g)
+                : launch_t<VPL, double, 1, false, U8>(a, num_sms, mg, s, g);
   }
   if (accum == 2) {
-    if (metric == 0) return full ? launch_t<VPL, F2, 0, true>(a, num_sms, mg, s, g)
-                                 : launch_t<VPL, F2, 0, false>(a, num_sms, mg, s, g);
-    return full ? launch_t<VPL, F2, 1, true>(a, num_sms, mg, s, g)
-                : launch_t<VPL, F2, 1, false>(a, num_sms, mg, s, g);
+    if (metric == 0) return full ? launch_t<VPL, F2, 0, true, U8>(a, num_sms, mg, s, g)
+                                 : launch_t<VPL, F2, 0, false, U8>(a, num_sms, mg, s, g);
+    return full ? launch_t<VPL, F2, 1, true, U8>(a, num_sms, mg, s, g)
+                : launch_t<VPL, F2, 1, false, U8>(a, num_sms, mg, s, g);
   }
-  if (metric == 0) return full ? launch_t<VPL, float, 0, true>(a, num_sms, mg, s, g)
-                               : launch_t<VPL, float, 0, false>(a, num_sms, mg, s, g);
-  return full ? launch_t<VPL, float, 1, true>(a, num_sms, mg, s, g)
-              : launch_t<VPL, float, 1, false>(a, num_sms, mg, s, g);
+  if (metric == 0) return full ? launch_t<VPL, float, 0, true, U8>(a, num_sms, mg, s, g)
+                               : launch_t<VPL, float, 0, false, U8>(a, num_sms, mg, s, g);
+  return full ? launch_t<VPL, float, 1, true, U8>(a, num_sms, mg, s, g)
+              : launch_t<VPL, float, 1, false, U8>(a, num_sms, mg, s, g);
 }
 
 }  // namespace
@@ -380,17 +408,42 @@ size_t search_smem_bytes(int cap, int chp, int beam, int hsize, bool hash_in_sme
 cudaError_t launch_search(const SearchArgs& a, int metric, int accum, int num_sms,
                           int max_grid, cudaStream_t stream, int* grid_out) {
   const int vpl = (a.dpad + 127) / 128;
+  if (a.vectors8) {  // byte storage: the rows of byte datasets (SIFT, Deep: dim <= 256)
+    switch (vpl) {
+      case 1: return launch_v<1, true>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+      case 2: return launch_v<2, true>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (vpl) {
-    case 1: return launch_v<1>(a, metric, accum, num_sms, max_grid, stream, grid_out);
-    case 2: return launch_v<2>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 1: return launch_v<1, false>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 2: return launch_v<2, false>(a, metric, accum, num_sms, max_grid, stream, grid_out);
     case 3:
-    case 4: return launch_v<4>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 4: return launch_v<4, false>(a, metric, accum, num_sms, max_grid, stream, grid_out);
     case 5:
-    case 6: return launch_v<6>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 6: return launch_v<6, false>(a, metric, accum, num_sms, max_grid, stream, grid_out);
     case 7:
-    case 8: return launch_v<8>(a, metric, accum, num_sms, max_grid, stream, grid_out);
+    case 8: return launch_v<8, false>(a, metric, accum, num_sms, max_grid, stream, grid_out);
     default: return cudaErrorInvalidValue;
   }
+}
+
+namespace {
+__global__ void to_u8_kernel(const float* __restrict__ x, uint64_t n, uint8_t* __restrict__ out, int* bad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    const bool ok = v >= 0.f && v <= 255.f && v == rintf(v);
+    if (!ok) atomicOr(bad, 1);
+    out[i] = ok ? (uint8_t)v : 0;
+  }
+}
+}  // namespace
+
+cudaError_t launch_to_u8(const float* x, uint64_t n, uint8_t* out, int* bad, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 32);
+  to_u8_kernel<<<(unsigned)blocks, 256, 0, stream>>>(x, n, out, bad);
+  return cudaGetLastError();
 }
 
 }  // namespace dvsg

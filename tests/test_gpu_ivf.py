@@ -306,3 +306,35 @@ def test_ivf_graph_tensor_cores_equal_cuda_cores(ctx):
         graphs.append(ctx_adjacency(ctx, 40000, 32).copy())
     assert np.array_equal(graphs[0], graphs[1])
     ctx.reset()
+
+
+def test_u8_vector_storage_bit_identical(ctx, oracle):
+    """dvsg_set_vector_storage(U8): K1 gathers a byte copy of the rows; ids,
+    distances, counts and visited equal the f32-storage search (and the
+    oracle) in every accumulation mode; float data is refused; the copy is
+    dropped when the rows change."""
+    from conftest import sift_like
+    x = sift_like(6000, 96, 8, 21)
+    q = sift_like(300, 96, 8, 22) + 0.25  # float queries: only the rows must be bytes
+    adj = oracle.build_graph(x, 16)
+    eo = oracle.compute_entry_order(x)
+    ctx.reset()
+    ctx.load_partition(0, dvs.GraphIndex(x, np.arange(len(x), dtype=np.uint32), 16, adj, eo))
+    for accum in ("f32", "f64", "f32c"):
+        p = dvs.SearchParams(8, 32, 10, 32, accum=accum)
+        ctx.set_vector_storage("f32")
+        a = ctx.beam_search(0, q, p)
+        ctx.set_vector_storage("u8")
+        b = ctx.beam_search(0, q, p)
+        for u, v in zip(a, b):
+            assert np.array_equal(u, v), accum
+    want = oracle.beam_search(x, np.arange(len(x), dtype=np.uint32), adj, eo, q, 8, 32, 10, 32)
+    got = ctx.beam_search(0, q, dvs.SearchParams(8, 32, 10, 32, accum="f64"))
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    ctx.set_vector_storage("f32")
+    xf = x + 0.5
+    ctx.reset()
+    ctx.load_partition(0, dvs.GraphIndex(xf, np.arange(len(x), dtype=np.uint32), 16, adj, eo))
+    with pytest.raises(dvs.InvalidArgument):
+        ctx.set_vector_storage("u8")
+    ctx.reset()
