@@ -2,7 +2,7 @@
 """bench.py -- QPS of the batched graph search at recall@10 >= 0.95 on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dvsg|reference]
-                    [--workload cfg3|cfg1]
+                    [--workload cfg3|cfg1|cfg4]
 
 Workloads (BASELINE.json configs):
   cfg3 (default) -- configs[2], the north-star config: Deep-like synthetic
@@ -12,6 +12,8 @@ Workloads (BASELINE.json configs):
         per step, top-10, beam 16, I=24, entry 16 (calibrated: recall@10
         >= 0.95 against brute-force ground truth on a 2,000-query sample).
   cfg1 -- configs[1] at N=1: 1M x 128, exact kNN-32 graph, 100k queries, I=6.
+  cfg4 -- configs[3]: text-embedding-like 10M x 768 float, inner product,
+        top-100, beam 256, I=16, 100k queries per GPU (f64 parity mode).
 
 One step = one run_pipeline pass (simulator.cpp:245-337, functional part:
 assign -> route -> K1 beam search -> combine -> attach hit vectors) over one
@@ -32,6 +34,9 @@ scaling); full-replica searches are measured beside it.
               SURVEY 8d) / K1 event time, against MEASURED_PEAKS.json hbm_gbs;
               `traffic` = ncu dram__bytes of K1 on the same config
               (profiles/k1_traffic.json; ncu cannot run inside the timed run).
+`accum_modes`, `storage_u8`: side measurements of the same search (f64 /
+              f32c accumulation; K1 on a byte copy of the rows) with their
+              ids compared to the headline's.
 `cpu_baseline`: the reference's own run_pipeline (oracle/_ref, compiled from
               /root/reference sources) on a bounded query sample, all host cores.
 `--impl reference`: rank 0 times the reference's run_pipeline on the same
