@@ -164,7 +164,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) {
     top[rr] = ~0ull;
-    if ((flags & 4) && grp == 0) {  // continue from the lists already in the output
+    if (flags & 4) {  // continue from the lists already in the output (group 1: their m-th key only)
       const uint64_t o = __shfl_sync(0xFFFFFFFFu, orow, rr);
       const bool v = __shfl_sync(0xFFFFFFFFu, rvalid, rr);
       uint32_t id = 0xFFFFFFFFu;
@@ -175,8 +175,9 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
       }
       const unsigned bad = __ballot_sync(0xFFFFFFFFu, id == 0xFFFFFFFFu);
       const int first_bad = bad ? __ffs(bad) - 1 : 32;  // entries after the first gap are ignored
-      if (lane < first_bad) top[rr] = ((uint64_t)f2ord(d) << 32) | id;
-      const uint64_t t = __shfl_sync(0xFFFFFFFFu, top[rr], m - 1);
+      const uint64_t prev = lane < first_bad ? ((uint64_t)f2ord(d) << 32) | id : ~0ull;
+      if (grp == 0) top[rr] = prev;  // group 1 keeps an empty list (no duplicates at the hand-over)
+      const uint64_t t = __shfl_sync(0xFFFFFFFFu, prev, m - 1);
       if (lane == rr) set_thr(t);
     }
   }
@@ -313,20 +314,21 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
     }
     __syncthreads();
     if (grp == 0) {
+      // merge two ascending 32-lists: min with the other list reversed is a
+      // bitonic sequence holding the 32 smallest of the union; 5 half-cleaner
+      // stages sort it (no per-key insertion)
       const uint64_t* other = cbuf0 + 32 * TCM;
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr) {
         const int row = rw * 32 + rr;
-        for (int s2 = 0; s2 < 32; ++s2) {
-          const uint64_t key = other[s2 * TCM + row];
-          if (key == ~0ull) break;  // sorted: the rest are empty
-          const unsigned gt = __ballot_sync(0xFFFFFFFFu, top[rr] > key);
-          if (gt == 0) break;  // sorted: no later key can enter either
-          const int pos = __ffs(gt) - 1;
-          const uint64_t up = __shfl_up_sync(0xFFFFFFFFu, top[rr], 1);
-          if (lane > pos) top[rr] = up;
-          if (lane == pos) top[rr] = key;
+        const uint64_t o = other[(31 - lane) * TCM + row];
+        uint64_t v = top[rr] < o ? top[rr] : o;
+#pragma unroll
+        for (int j = 16; j > 0; j >>= 1) {
+          const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+          v = (lane & j) ? (w > v ? w : v) : (w < v ? w : v);
         }
+        top[rr] = v;
       }
     }
   }
@@ -389,10 +391,13 @@ cudaError_t launch_tc_g(const T* rows, const float* rnorm, const T* cols, const 
   return cudaGetLastError();
 }
 
-// groups: 2 pays a fixed hand-over merge per block and a second list warm-up;
-// it wins on long column lists (large-C assign: 32 tiles per block, 60 -> 51 ms
-// at 1M x 4096) and loses on the graph build's short merged passes (~9 tiles
-// per block: 8.2 -> 20.5 s of kNN at 100M), so each caller picks.
+// groups: a second epilogue group doubles the warps per CTA but its survivor
+// buffer costs 32 KB of smem.  When one group already fits two CTAs per SM
+// (bf16 build rows: 106 KB) the second CTA hides the load / MMA / epilogue
+// phases better than more warps in one CTA (two groups: 1 CTA/SM, 8.2 ->
+// 17.5 s of kNN at 100M); when one group is already alone on its SM (TF32
+// assign rows: 176 KB) the second group is free (1M x 4096: 60 -> 48 ms).
+// groups = 0: that rule; DVSG_TC_GROUPS overrides.
 template <typename T>
 cudaError_t launch_tc_t(const T* rows, const float* rnorm, const T* cols, const float* cnorm, int kpad,
                         const uint32_t* row_map, const RangeBlock* blocks, uint64_t nblocks, const uint32_t* list_off,
@@ -406,6 +411,7 @@ cudaError_t launch_tc_t(const T* rows, const float* rnorm, const T* cols, const 
     return e ? std::atoi(e) : 0;
   }();
   if (groups_env > 0) groups = groups_env;
+  if (groups == 0) groups = 2 * tc_smem_bytes(row_bytes, 1) + 2048 > 227 * 1024 ? 2 : 1;
   // two epilogue groups only if their second survivor buffer fits (227 KB opt-in)
   if (groups >= 2 && tc_smem_bytes(row_bytes, 2) + 2048 <= 227 * 1024)
     return launch_tc_g<T, 2>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
@@ -420,7 +426,7 @@ cudaError_t launch_range_topk_tc(const uint16_t* rows, const float* rnorm, const
                                  float* out_dists, uint64_t out_stride, cudaStream_t stream) {
   if (kpad % 16) return cudaErrorInvalidValue;
   return launch_tc_t<uint16_t>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
-                               out_ids, out_dists, out_stride, 1, stream);
+                               out_ids, out_dists, out_stride, 0, stream);
 }
 
 cudaError_t launch_range_topk_tf32(const float* rows, const float* rnorm, const float* cols, const float* cnorm,
@@ -429,7 +435,7 @@ cudaError_t launch_range_topk_tf32(const float* rows, const float* rnorm, const 
                                    float* out_dists, uint64_t out_stride, cudaStream_t stream) {
   if (kpad % 8) return cudaErrorInvalidValue;
   return launch_tc_t<float>(rows, rnorm, cols, cnorm, kpad, row_map, blocks, nblocks, list_off, ranges, m, flags,
-                            out_ids, out_dists, out_stride, 2, stream);
+                            out_ids, out_dists, out_stride, 0, stream);
 }
 
 cudaError_t launch_to_bf16(const float* x, uint64_t n, int dpad, int kpad, uint16_t* out, cudaStream_t stream) {
