@@ -7,6 +7,7 @@ set -u
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 OUT=$ROOT/gpurun_out/stress; mkdir -p $OUT
 LIB=$ROOT/paper_2512_02278_b200/variants/libdvsg_stress.so
+mkdir -p "$(dirname "$LIB")"
 if [ ! -f "$LIB" ]; then
   make -s -C $ROOT/paper_2512_02278_b200/csrc -j8 OUT=$LIB OBJ=$ROOT/build/obj_stress EXTRA=-DDVSG_STRESS=1 > $OUT/build.log 2>&1
 fi
