@@ -715,3 +715,25 @@ def test_compensated_f32_sharded_equals_unsharded(ctx, oracle, exchange, metric,
     finally:
         ctx.set_shard_exchange("bulk")
     _assert_same(got, want, True, f"f32c sharded {exchange} {metric}")
+
+
+@pytest.mark.parametrize("dim", [300, 512, 640, 1024])
+@pytest.mark.parametrize("accum", ["f64", "f32"])
+def test_wide_rows_match_oracle(ctx, oracle, dim, accum):
+    """Wide-row K1 (VPL 3-8: 4 or 2 rows in flight per warp at 2 CTAs/SM,
+    FULL and padded rows) against the oracle.  f64 on float data: exact by
+    construction (rounding-boundary guard); f32 on byte data: exact sums."""
+    rng = np.random.default_rng(dim)
+    n, nq = 3000, 200
+    if accum == "f64":
+        v = rng.normal(size=(n, dim)).astype(np.float32)
+        q = rng.normal(size=(nq, dim)).astype(np.float32)
+    else:
+        v = rng.integers(0, 16, size=(n, dim)).astype(np.float32)  # partial sums stay below 2^24
+        q = rng.integers(0, 16, size=(nq, dim)).astype(np.float32)
+    adj = oracle.build_graph(v, 16)
+    eo = oracle.compute_entry_order(v)
+    gids = np.arange(n, dtype=np.uint32)
+    want = oracle.beam_search(v, gids, adj, eo, q, 5, 48, 10, 48)
+    got = _search(ctx, v, adj, q, dvs.SearchParams(5, 48, 10, 48, accum=accum), eo=eo)
+    _assert_same(got, want, True, f"dim={dim} {accum}")
