@@ -737,3 +737,24 @@ def test_wide_rows_match_oracle(ctx, oracle, dim, accum):
     want = oracle.beam_search(v, gids, adj, eo, q, 5, 48, 10, 48)
     got = _search(ctx, v, adj, q, dvs.SearchParams(5, 48, 10, 48, accum=accum), eo=eo)
     _assert_same(got, want, True, f"dim={dim} {accum}")
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_sharded_wide_rows_f64_exact(ctx, oracle, nranks):
+    """Node-sharded scorer on wide rows (768-d: 4 rows in flight per warp) in
+    the f64 mode on float data: identical to K1 and to the oracle."""
+    rng = np.random.default_rng(77 + nranks)
+    n, nq, dim = 3000, 120, 768
+    v = rng.normal(size=(n, dim)).astype(np.float32)
+    q = rng.normal(size=(nq, dim)).astype(np.float32)
+    adj = oracle.build_graph(v, 16)
+    eo = oracle.compute_entry_order(v)
+    p = dvs.SearchParams(5, 32, 10, 32, accum="f64")
+    k1 = _search(ctx, v, adj, q, p, eo=eo)
+    for mode in ("bulk", "fused"):
+        ctx.set_shard_exchange(mode)
+        got = ctx.beam_search_sharded_emulated(nranks, q, p)
+        _assert_same(got, k1, True, f"sharded {mode} R={nranks}")
+    ctx.set_shard_exchange("bulk")
+    want = oracle.beam_search(v, np.arange(n, dtype=np.uint32), adj, eo, q, 5, 32, 10, 32)
+    _assert_same(k1, want, True, "k1 vs oracle")
