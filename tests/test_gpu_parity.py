@@ -758,3 +758,16 @@ def test_sharded_wide_rows_f64_exact(ctx, oracle, nranks):
     ctx.set_shard_exchange("bulk")
     want = oracle.beam_search(v, np.arange(n, dtype=np.uint32), adj, eo, q, 5, 32, 10, 32)
     _assert_same(k1, want, True, "k1 vs oracle")
+
+
+def test_brute_force_float_tiny_and_k_equals_n(ctx, ref):
+    """Exact-mode brute force where every row is a candidate (n <= 32, k = n)
+    and where k is the last valid size."""
+    rng = np.random.default_rng(12)
+    for n, k in ((5, 5), (32, 32), (33, 32), (40, 1)):
+        v = rng.normal(size=(n, 9)).astype(np.float32)
+        q = rng.normal(size=(7, 9)).astype(np.float32)
+        wi, wd = ref.brute_force_topk(v, q, k)
+        gi, gd = ctx.brute_force_topk(v, q, k)
+        assert ctx.last_knn_info()[0] == 1
+        assert np.array_equal(gi, wi) and np.array_equal(gd, wd), (n, k)
