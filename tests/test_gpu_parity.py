@@ -340,6 +340,32 @@ def test_assign_large_c_tiled_matches_reference(ctx, oracle, clusters, dim, c):
     assert np.array_equal(got, want)
 
 
+def test_pipeline_pinned_and_pageable_schedules_agree(ctx, golden):
+    """dvsg_run_pipeline picks its copy schedule from the host buffers
+    (pinned: all H2D first; pageable: interleaved); both equal the golden."""
+    import torch
+    from fnsy import G3_FNSY
+    res = golden("g3_mixture.npz")
+    dvs.load_index(G3_FNSY, ctx=ctx)
+    q = res["queries"]
+    nq, dim = q.shape
+    k = 10
+    pq = torch.empty((nq, dim), dtype=torch.float32).pin_memory().numpy()
+    pq[:] = q
+    out = {"ids": torch.empty((nq, k), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+           "dists": torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy(),
+           "counts": torch.empty((nq,), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+           "vectors": torch.empty((nq, k, dim), dtype=torch.float32).pin_memory().numpy()}
+    p = dvs.SearchParams(6, 16, 10, 16)
+    pinned = ctx.run_pipeline(pq, p, 2, 4, batch_index=1, out=out)
+    pageable = ctx.run_pipeline(q.copy(), p, 2, 4, batch_index=1)
+    for a, b in ((pinned.ids, pageable.ids), (pinned.dists, pageable.dists), (pinned.counts, pageable.counts),
+                 (pinned.hit_vectors, pageable.hit_vectors)):
+        assert np.array_equal(a, b)
+    assert np.array_equal(pinned.counts, res["counts_f2"])
+    assert pinned.visited_total == pageable.visited_total == int(res["visited_f2"])
+
+
 def test_pipeline_matches_reference_golden(ctx, golden):
     from fnsy import G3_FNSY
     res = golden("g3_mixture.npz")
