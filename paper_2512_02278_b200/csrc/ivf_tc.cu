@@ -56,6 +56,19 @@ __device__ __forceinline__ float ord2f(uint32_t o) {
   return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
+// the 32 smallest of two ascending 32-lists (lane i holds entry i of each):
+// min against the reversed other list is bitonic; 5 half-cleaners sort it
+__device__ __forceinline__ uint64_t warp_merge_u64(uint64_t a, uint64_t b_sorted, int lane) {
+  const uint64_t rev = __shfl_sync(0xFFFFFFFFu, b_sorted, 31 - lane);
+  uint64_t v = a < rev ? a : rev;
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+    v = (lane & j) ? (w > v ? w : v) : (w < v ? w : v);
+  }
+  return v;
+}
+
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
                : "memory");
@@ -160,7 +173,15 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
   // short, so the padding columns (+inf) never pass
   const uint64_t kInfKey = (uint64_t)f2ord(__int_as_float(0x7F800000)) << 32;
   uint64_t thr = kInfKey;
-  auto set_thr = [&](uint64_t t) { thr = t == ~0ull ? kInfKey : t; };
+  // two groups: each publishes its rows' m-th keys; a column that fails the
+  // other group's key cannot reach the union's top m either, so each group
+  // filters with the smaller of the two (stale values are larger: safe)
+  __shared__ uint64_t gthr[G][TCM];
+  gthr[grp][rt] = kInfKey;
+  auto set_thr = [&](uint64_t t) {
+    thr = t == ~0ull ? kInfKey : t;
+    if (G == 2) gthr[grp][rt] = thr;
+  };
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) {
     top[rr] = ~0ull;
@@ -266,6 +287,11 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       // (1) this thread's row: survivors of the m-th-key filter -> cbuf
       int ns = 0;
+      uint64_t fthr = thr;
+      if (G == 2) {
+        const uint64_t o = gthr[grp ^ 1][rt];
+        fthr = o < fthr ? o : fthr;
+      }
       if (rvalid) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -273,7 +299,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
           const uint32_t col = tc + (uint32_t)cl;
           const float dist = fmaxf(fmaf(-2.f, __uint_as_float(r[j]), nr + cn[buf][cl]), 0.f);
           const uint64_t key = ((uint64_t)f2ord(dist) << 32) | col;
-          const bool ok = key < thr && !((flags & 1) && col == prow);
+          const bool ok = key < fthr && !((flags & 1) && col == prow);
           if (ok) cbuf[ns * TCM + rt] = key;
           ns += ok ? 1 : 0;
         }
@@ -321,14 +347,7 @@ range_topk_tc_kernel(const T* __restrict__ rows, const float* __restrict__ rnorm
 #pragma unroll
       for (int rr = 0; rr < 32; ++rr) {
         const int row = rw * 32 + rr;
-        const uint64_t o = other[(31 - lane) * TCM + row];
-        uint64_t v = top[rr] < o ? top[rr] : o;
-#pragma unroll
-        for (int j = 16; j > 0; j >>= 1) {
-          const uint64_t w = __shfl_xor_sync(0xFFFFFFFFu, v, j);
-          v = (lane & j) ? (w > v ? w : v) : (w < v ? w : v);
-        }
-        top[rr] = v;
+        top[rr] = warp_merge_u64(top[rr], other[lane * TCM + row], lane);
       }
     }
   }
