@@ -827,7 +827,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        return run_reference_impl(args, world, rank)
+        # rank 0 times the CPU reference; the line carries the N of the run
+        # (torchrun's WORLD_SIZE, or --gpus when launched without torchrun)
+        return run_reference_impl(args, max(world, args.gpus), rank)
 
     import torch
     import paper_2512_02278_b200 as dvs
